@@ -1,0 +1,774 @@
+// LP builder (kernels K1-K3): graph edge list -> standard-form
+// LP in HBM (CSC with sign-bit coefficients, unique edge rows, costs, bounds), the
+// initial point z0 with r0 = A z0 - b, and max ||a_j||^2 for L_max (Eq. 7).
+//
+//   VC  (Eq. 2):   row e = (u < v): x_u + x_v - s_e = 1
+//   MIS (App. B.2):           row e:           x_u + x_v + s_e = 1, max w^T x
+//   MWC (App. B.3): x_v^l at v*k+l, x_e^l at n*k+e*k+l;
+//        row 2(ek+l):   x_e^l + x_u^l - x_v^l - s = 0
+//        row 2(ek+l)+1: x_e^l - x_u^l + x_v^l - s = 0
+//
+// Sort / unique / scan steps use CUB (header-only, part of the CUDA toolkit);
+// every LP-specific step is a kernel below.
+#include <cub/cub.cuh>
+
+#include "thetis_internal.cuh"
+
+namespace thetis {
+
+namespace {
+
+constexpr int T = 256;
+
+enum Flag { FLAG_BAD_INPUT = 0, FLAG_DUP_TERMINAL = 1, FLAG_BAD_CSC = 2, FLAG_BAD_CSR = 3, FLAG_BAD_BOUNDS = 4 };
+
+// ---------------------------------------------------------------- K1: keys
+__global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ src,
+                            const int32_t* __restrict__ dst, uint64_t* __restrict__ keys,
+                            int32_t* __restrict__ idx, int32_t* flags) {
+    const uint64_t sent = (uint64_t)n * (uint64_t)n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t u = src[i], v = dst[i];
+        if (u < 0 || v < 0 || u >= n || v >= n) {
+            atomicOr(&flags[FLAG_BAD_INPUT], 1);
+            keys[i] = sent;
+        } else if (u == v) {
+            keys[i] = sent; // self-loop: sorts last, dropped
+        } else {
+            uint64_t a = (uint64_t)(u < v ? u : v), b = (uint64_t)(u < v ? v : u);
+            keys[i] = a * (uint64_t)n + b;
+        }
+        if (idx) idx[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_decode_edges(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[e];
+        edges[e] = make_int2((int32_t)(k / (uint64_t)n), (int32_t)(k % (uint64_t)n));
+    }
+}
+// (v, e) pairs for the stable by-v sort (lower incidences)
+__global__ void k_vkeys(int64_t m, const int2* __restrict__ edges, int32_t* __restrict__ vkey, int32_t* __restrict__ eval) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        vkey[e] = edges[e].y;
+        eval[e] = (int32_t)e;
+    }
+}
+
+// run boundaries of a sorted key sequence: start[key] = first pos, end[key] = last pos + 1
+__global__ void k_runs_u(int64_t m, const int2* __restrict__ edges, int32_t* start, int32_t* end) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        int u = edges[e].x;
+        if (e == 0 || edges[e - 1].x != u) start[u] = (int32_t)e;
+        if (e == m - 1 || edges[e + 1].x != u) end[u] = (int32_t)(e + 1);
+    }
+}
+__global__ void k_runs_key(int64_t m, const int32_t* __restrict__ key, int32_t* start, int32_t* end) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        int v = key[p];
+        if (p == 0 || key[p - 1] != v) start[v] = (int32_t)p;
+        if (p == m - 1 || key[p + 1] != v) end[v] = (int32_t)(p + 1);
+    }
+}
+__global__ void k_degrees(int64_t n, const int32_t* us, const int32_t* ue, const int32_t* ls, const int32_t* le,
+                          int64_t* deg) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x)
+        deg[v] = v < n ? (int64_t)(ue[v] - us[v]) + (int64_t)(le[v] - ls[v]) : 0;
+}
+// incidence lists in ascending edge order: lower incidences (v = ev[e]) come
+// first (their rows precede the upper run of v), then the upper run.
+__global__ void k_fill_lower(int64_t m, const int32_t* __restrict__ vkey, const int32_t* __restrict__ eval,
+                             const int32_t* __restrict__ ls, const int64_t* __restrict__ iptr, int32_t* inc) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        int v = vkey[p];
+        inc[iptr[v] + (p - ls[v])] = eval[p];
+    }
+}
+__global__ void k_fill_upper(int64_t m, const int2* __restrict__ edges, const int32_t* __restrict__ us,
+                             const int32_t* __restrict__ ls, const int32_t* __restrict__ le,
+                             const int64_t* __restrict__ iptr, int32_t* inc) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        int u = edges[e].x;
+        inc[iptr[u] + (le[u] - ls[u]) + (e - us[u])] = (int32_t)e;
+    }
+}
+
+__global__ void k_max_deg(int64_t n, const int64_t* __restrict__ colptr, unsigned long long* out) {
+    unsigned long long best = 0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long d = (unsigned long long)(colptr[j + 1] - colptr[j]);
+        best = d > best ? d : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+        best = x > best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// ---------------------------------------------------------------- MWC
+__global__ void k_gather_ew(int64_t m, const int32_t* __restrict__ first, const float* __restrict__ ew_in,
+                            float* __restrict__ ew) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+        ew[e] = ew_in[first[e]];
+}
+
+__global__ void k_mwc_colptr(int64_t n, int64_t m, int k, const int64_t* __restrict__ iptr, int64_t* colptr) {
+    const int64_t nk = n * k, ns = nk + m * k;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= ns; j += (int64_t)gridDim.x * blockDim.x) {
+        if (j < nk) {
+            int64_t v = j / k, l = j % k;
+            int64_t deg = iptr[v + 1] - iptr[v];
+            colptr[j] = 2 * (int64_t)k * iptr[v] + 2 * l * deg;
+        } else {
+            colptr[j] = 4 * (int64_t)k * m + 2 * (j - nk);
+        }
+    }
+}
+__global__ void k_mwc_fill_vertex(int64_t n, int k, const int64_t* __restrict__ iptr, const int32_t* __restrict__ inc,
+                                  const int2* __restrict__ edges, const int64_t* __restrict__ colptr,
+                                  int32_t* __restrict__ rowidx) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t p = iptr[v]; p < iptr[v + 1]; p++) {
+            int64_t e = inc[p], q = p - iptr[v];
+            bool lower = edges[e].x == (int32_t)v;
+            for (int l = 0; l < k; l++) {
+                int64_t base = colptr[v * k + l] + 2 * q;
+                uint32_t r0 = (uint32_t)(2 * (e * k + l)), r1 = r0 + 1;
+                rowidx[base] = (int32_t)(lower ? r0 : (r0 | kSignBit));
+                rowidx[base + 1] = (int32_t)(lower ? (r1 | kSignBit) : r1);
+            }
+        }
+    }
+}
+__global__ void k_mwc_fill_edge(int64_t m, int k, int64_t nnz_vertex, int32_t* __restrict__ rowidx,
+                                const float* __restrict__ ew, float* __restrict__ c, int64_t nk) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m * k; q += (int64_t)gridDim.x * blockDim.x) {
+        rowidx[nnz_vertex + 2 * q] = (int32_t)(2 * q);
+        rowidx[nnz_vertex + 2 * q + 1] = (int32_t)(2 * q + 1);
+        c[nk + q] = ew[q / k] * 0.5f; // objective (1/2) sum_e c_e sum_l x_e^l
+    }
+}
+__global__ void k_mwc_terminals(int64_t n, int k, int t, const int32_t* __restrict__ terms, int32_t* term_label,
+                                int32_t* flags) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)k * t) return;
+    int32_t v = terms[i];
+    if (v < 0 || v >= n) { atomicOr(&flags[FLAG_BAD_INPUT], 1); return; }
+    if (atomicCAS(&term_label[v], -1, (int32_t)(i / t)) != -1) atomicOr(&flags[FLAG_DUP_TERMINAL], 1);
+}
+// initial point (R-3): free blocks at the simplex barycentre, terminal blocks at e_l
+__global__ void k_mwc_init(int64_t n, int k, const int32_t* __restrict__ term_label, float* __restrict__ z,
+                           uint8_t* __restrict__ unit_fixed, int64_t S) {
+    const float bary = (float)(1.0 / (double)k);
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
+        if (u < n) {
+            int tl = term_label[u];
+            unit_fixed[u] = tl >= 0;
+            for (int l = 0; l < k; l++) z[u * k + l] = tl >= 0 ? (l == tl ? 1.0f : 0.0f) : bary;
+        } else {
+            unit_fixed[u] = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- generic
+__global__ void k_check_csc(int64_t n, int64_t m, int64_t nnz, const int64_t* __restrict__ colptr,
+                            const int32_t* __restrict__ rowidx, int32_t* flags, int flag) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = colptr[j], b = colptr[j + 1];
+        if ((j == 0 && a != 0) || (j == n - 1 && b != nnz) || b < a || a < 0 || b > nnz) {
+            atomicOr(&flags[flag], 1);
+            continue;
+        }
+        for (int64_t t = a; t < b; t++) {
+            int32_t i = rowidx[t];
+            if (i < 0 || i >= m || (t > a && i <= rowidx[t - 1])) { atomicOr(&flags[flag], 1); break; }
+        }
+    }
+}
+// order-independent fingerprint of the entry set, to check CSC == CSR
+__device__ __forceinline__ unsigned long long entry_hash(int64_t i, int64_t j, float v) {
+    return sm64_mix(((uint64_t)i << 32 | (uint64_t)(uint32_t)j) ^ ((uint64_t)__float_as_uint(v) * 0x9E3779B97F4A7C15ULL));
+}
+__global__ void k_fp_csc(int64_t n, const int64_t* colptr, const int32_t* rowidx, const float* val,
+                         unsigned long long* out) {
+    unsigned long long h = 0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t t = colptr[j]; t < colptr[j + 1]; t++) h += entry_hash(rowidx[t], j, val ? val[t] : 1.0f);
+    atomicAdd(out, h);
+}
+__global__ void k_fp_csr(int64_t m, const int64_t* rowptr, const int32_t* rcol, const float* rval,
+                         unsigned long long* out) {
+    unsigned long long h = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t t = rowptr[i]; t < rowptr[i + 1]; t++) h += entry_hash(i, rcol[t], rval ? rval[t] : 1.0f);
+    atomicAdd(out, h);
+}
+__global__ void k_slack_flags(int64_t m, const int8_t* __restrict__ sense, int32_t* __restrict__ isq,
+                              int32_t* flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == m) { isq[i] = 0; continue; }
+        int s = sense[i];
+        if (s < 0 || s > 2) atomicOr(&flags[FLAG_BAD_INPUT], 1);
+        isq[i] = s != THETIS_EQ;
+    }
+}
+__global__ void k_slack_maps(int64_t m, int64_t n, const int8_t* __restrict__ sense, const int32_t* __restrict__ pos,
+                             int64_t* __restrict__ row_slack, int32_t* __restrict__ slack_row) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (sense[i] != THETIS_EQ) {
+            row_slack[i] = n + pos[i];
+            slack_row[pos[i]] = (int32_t)i;
+        } else {
+            row_slack[i] = -1;
+        }
+    }
+}
+__global__ void k_colnorm2(int64_t n, const int64_t* __restrict__ colptr, const float* __restrict__ val,
+                           double* __restrict__ out, unsigned long long* max_bits) {
+    double best = 0.0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t t = colptr[j]; t < colptr[j + 1]; t++) {
+            double v = val ? (double)val[t] : 1.0;
+            s += v * v;
+        }
+        if (out) out[j] = s;
+        best = s > best ? s : best;
+    }
+    // non-negative doubles order like their bit patterns
+    atomicMax(max_bits, (unsigned long long)__double_as_longlong(best));
+}
+__global__ void k_generic_init(int64_t n, int64_t n_blocks, int k, const float* __restrict__ lo,
+                               const float* __restrict__ hi, float* __restrict__ z, uint8_t* __restrict__ unit_fixed,
+                               int32_t* flags) {
+    const int64_t S = n_blocks + (n - n_blocks * k);
+    const float bary = k > 0 ? (float)(1.0 / (double)k) : 0.0f;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
+        int64_t f = u < n_blocks ? u * k : n_blocks * k + (u - n_blocks);
+        int64_t cnt = u < n_blocks ? k : 1;
+        bool fixed = true;
+        for (int64_t j = f; j < f + cnt; j++) {
+            float l = lo ? lo[j] : 0.0f, h = hi ? hi[j] : 1.0f;
+            if (!(l <= h)) atomicOr(&flags[FLAG_BAD_BOUNDS], 1);
+            fixed = fixed && (l == h);
+        }
+        unit_fixed[u] = fixed;
+        for (int64_t j = f; j < f + cnt; j++) {
+            float l = lo ? lo[j] : 0.0f, h = hi ? hi[j] : 1.0f;
+            float z0;
+            if (u < n_blocks && !fixed) {
+                z0 = bary;
+            } else {
+                z0 = 0.0f < l ? l : 0.0f;
+                z0 = z0 > h ? h : z0;
+            }
+            z[j] = z0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- r0, ua
+// r_i = -b_i + sum_j a_ij z_j (ascending columns) + sigma_i s_i, row-sequential fp32
+__global__ void k_recompute_r(DevLP L) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = -row_b(L, i);
+        if (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) {
+            int2 e = L.edges[i];
+            acc = __fadd_rn(acc, L.z[e.x]);
+            acc = __fadd_rn(acc, L.z[e.y]);
+        } else if (L.problem == THETIS_PROB_MWC) {
+            int64_t k = L.k, e = i / (2 * k), rem = i % (2 * k), l = rem >> 1;
+            bool second = rem & 1;
+            int2 uv = L.edges[e];
+            float zu = L.z[(int64_t)uv.x * k + l], zv = L.z[(int64_t)uv.y * k + l];
+            float ze = L.z[L.n_vert * k + e * k + l];
+            acc = __fadd_rn(acc, second ? -zu : zu);
+            acc = __fadd_rn(acc, second ? zv : -zv);
+            acc = __fadd_rn(acc, ze);
+        } else {
+            for (int64_t t = L.rowptr[i]; t < L.rowptr[i + 1]; t++) {
+                float a = L.rval ? L.rval[t] : 1.0f;
+                acc = __fadd_rn(acc, __fmul_rn(a, L.z[L.rcol[t]]));
+            }
+        }
+        int64_t sl = row_slack_of(L, i);
+        if (sl >= 0) acc = __fadd_rn(acc, __fmul_rn(row_sigma(L, i), L.z[sl]));
+        L.r[i] = acc;
+    }
+}
+// ua_j = ubar^T a_j, sequential over the column (same contract as the gradient dot)
+__global__ void k_recompute_ua(DevLP L) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < L.n_s; j += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        if (L.ubar)
+            for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) {
+                int64_t row;
+                float a;
+                entry(L, t, row, a);
+                acc = __fadd_rn(acc, __fmul_rn(a, L.ubar[row]));
+            }
+        L.ua[j] = acc;
+    }
+}
+
+int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) b++;
+    return b < 1 ? 1 : b;
+}
+
+struct GraphTemps {
+    uint64_t *keys, *keys2;
+    int32_t *idx, *idx2;
+    int32_t *vkey, *vkey2, *eval, *eval2;
+    int32_t *us, *ue, *ls, *le;
+    int64_t* deg;
+    int64_t* iptr;   // MWC: vertex incidence pointers
+    int32_t* inc;    // MWC: incidence lists
+    float* ew_in;
+    int32_t* terms;
+    int32_t *src_stage, *dst_stage;
+    void* cub;
+    size_t cub_bytes;
+    int64_t* nsel;
+};
+
+size_t cub_bytes_graph(int64_t n, int64_t E, bool pairs) {
+    size_t mx = 0, b = 0;
+    cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> di(nullptr, nullptr);
+    if (pairs) cub::DeviceRadixSort::SortPairs(nullptr, b, dk, di, E, 0, 64);
+    else cub::DeviceRadixSort::SortKeys(nullptr, b, dk, E, 0, 64);
+    mx = b > mx ? b : mx;
+    b = 0;
+    if (pairs)
+        cub::DeviceSelect::UniqueByKey(nullptr, b, (uint64_t*)nullptr, (int32_t*)nullptr, (uint64_t*)nullptr,
+                                       (int32_t*)nullptr, (int64_t*)nullptr, E);
+    else
+        cub::DeviceSelect::Unique(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, E);
+    mx = b > mx ? b : mx;
+    b = 0;
+    cub::DoubleBuffer<int32_t> dv(nullptr, nullptr), de(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, dv, de, E, 0, 32);
+    mx = b > mx ? b : mx;
+    b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, n + 1);
+    mx = b > mx ? b : mx;
+    return mx;
+}
+
+// temporaries needed by the colouring (class lists) and the rounding passes
+size_t post_build_temp(int64_t S, int64_t n_struct, int64_t n_vert) {
+    size_t b = 0, mx = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, S, 0, 32);
+    mx = b;
+    size_t colour = 2 * 256 + 2 * (size_t)S * 4 + mx + 4 * 256;
+    size_t round = 8 * 256 + (size_t)n_struct * 4 + 2 * (size_t)n_vert + (size_t)64 * kRedBlocks * 8 + 64 * 8 + 64 + 32;
+    return colour > round ? colour : round;
+}
+
+}  // namespace
+
+
+// --------------------------------------------------------------------------
+// workspace layouts: the size query and the carve run the same code
+// --------------------------------------------------------------------------
+static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* lp, void* ws, GraphTemps* tp) {
+    const bool carve = lp != nullptr;
+    Carver C(carve ? ws : nullptr);
+    const bool mwc = problem == THETIS_PROB_MWC;
+    const int64_t K = mwc ? k : 1;
+    const int64_t n_s = mwc ? n * K + E * K : n;
+    const int64_t m = mwc ? 2 * K * E : E;
+    const int64_t nnz = mwc ? 6 * K * E : 2 * E;
+    const int64_t S = mwc ? n + E * K : n;
+    const int64_t U = S + m;
+    int64_t* colptr = C.take<int64_t>(n_s + 1);
+    int32_t* rowidx = C.take<int32_t>(nnz);
+    int2* edges = C.take<int2>(E);
+    float* c = C.take<float>(n_s);
+    float* z = C.take<float>(n_s + m);
+    float* r = C.take<float>(m);
+    float* ua = C.take<float>(n_s);
+    float* ew = mwc ? C.take<float>(E) : nullptr;
+    int32_t* term_label = mwc ? C.take<int32_t>(n) : nullptr;
+    uint8_t* unit_fixed = mwc ? C.take<uint8_t>(S) : nullptr;
+    int32_t* colour = C.take<int32_t>(S);
+    int32_t* members = C.take<int32_t>(S);
+    int32_t* heavy = C.take<int32_t>((U + kTile - 1) / kTile);
+    double* red = C.take<double>(kRedBlocks * 16 + 256);
+    int32_t* flags = C.take<int32_t>(64);
+    // temporaries of the build, reused afterwards by colouring and rounding
+    size_t temp_start = (C.off + 255) & ~(size_t)255;
+    GraphTemps t{};
+    t.keys = C.take<uint64_t>(E);
+    t.keys2 = C.take<uint64_t>(E);
+    if (mwc) {
+        t.idx = C.take<int32_t>(E);
+        t.idx2 = C.take<int32_t>(E);
+        t.ew_in = C.take<float>(E);
+        t.terms = C.take<int32_t>(32 * 4096);
+        t.iptr = C.take<int64_t>(n + 1);
+        t.inc = C.take<int32_t>(2 * E);
+    }
+    t.us = C.take<int32_t>(n);
+    t.ue = C.take<int32_t>(n);
+    t.ls = C.take<int32_t>(n);
+    t.le = C.take<int32_t>(n);
+    t.deg = C.take<int64_t>(n + 1);
+    t.nsel = C.take<int64_t>(4);
+    t.cub_bytes = cub_bytes_graph(n, E, mwc);
+    t.cub = C.take<char>((int64_t)t.cub_bytes);
+    size_t total = C.off;
+    size_t post = post_build_temp(S, n_s, n);
+    if (temp_start + post > total) total = temp_start + post;
+    if (carve) {
+        DevLP& d = lp->d;
+        d.colptr = colptr; d.rowidx = rowidx; d.edges = edges; d.c = c; d.z = z; d.r = r; d.ua = ua;
+        d.ew = ew; d.term_label = term_label; d.unit_fixed = unit_fixed;
+        lp->colour = colour; lp->members = members; lp->heavy = heavy; lp->red = red; lp->flags = flags;
+        lp->temp = (char*)ws + temp_start;
+        lp->temp_bytes = total - temp_start;
+        // the by-v sort reuses the key double buffers (2 x 8E bytes); host
+        // inputs are staged in the second key buffer
+        t.vkey = (int32_t*)t.keys;
+        t.eval = (int32_t*)t.keys + E;
+        t.vkey2 = (int32_t*)t.keys2;
+        t.eval2 = (int32_t*)t.keys2 + E;
+        t.src_stage = (int32_t*)t.keys2;
+        t.dst_stage = (int32_t*)t.keys2 + E;
+        *tp = t;
+    }
+    return total + 256;
+}
+
+size_t graph_workspace(int problem, int64_t n, int64_t n_edges, int k, bool, thetis_lp*, void*) {
+    return graph_layout(problem, n, n_edges, k, nullptr, nullptr, nullptr);
+}
+
+static size_t generic_layout(int64_t m, int64_t n, int64_t nnz, bool has_val, thetis_lp* lp, void* ws,
+                             int32_t** scan_buf, void** cub_buf, size_t* cub_bytes) {
+    const bool carve = lp != nullptr;
+    Carver C(carve ? ws : nullptr);
+    const int64_t S = n; // upper bound on structural units
+    const int64_t U = n + m;
+    int64_t* colptr = C.take<int64_t>(n + 1);
+    int32_t* rowidx = C.take<int32_t>(nnz);
+    float* val = has_val ? C.take<float>(nnz) : nullptr;
+    double* colnorm2 = has_val ? C.take<double>(n) : nullptr;
+    int64_t* rowptr = C.take<int64_t>(m + 1);
+    int32_t* rcol = C.take<int32_t>(nnz);
+    float* rval = has_val ? C.take<float>(nnz) : nullptr;
+    float* b = C.take<float>(m);
+    int8_t* sense = C.take<int8_t>(m);
+    int64_t* row_slack = C.take<int64_t>(m);
+    int32_t* slack_row = C.take<int32_t>(m);
+    float* c = C.take<float>(n);
+    float* lo = C.take<float>(n);
+    float* hi = C.take<float>(n);
+    uint8_t* unit_fixed = C.take<uint8_t>(S);
+    float* z = C.take<float>(n + m);
+    float* r = C.take<float>(m);
+    float* ua = C.take<float>(n);
+    int32_t* colour = C.take<int32_t>(S);
+    int32_t* members = C.take<int32_t>(S);
+    int32_t* heavy = C.take<int32_t>((U + kTile - 1) / kTile);
+    double* red = C.take<double>(kRedBlocks * 16 + 256);
+    int32_t* flags = C.take<int32_t>(64);
+    size_t temp_start = (C.off + 255) & ~(size_t)255;
+    int32_t* scan = C.take<int32_t>(2 * (m + 1));
+    size_t cb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cb, (int32_t*)nullptr, (int32_t*)nullptr, m + 1);
+    void* cubp = C.take<char>((int64_t)cb);
+    size_t total = C.off;
+    size_t post = post_build_temp(S, n, 0);
+    if (temp_start + post > total) total = temp_start + post;
+    if (carve) {
+        DevLP& d = lp->d;
+        d.colptr = colptr; d.rowidx = rowidx; d.val = val; d.colnorm2 = colnorm2; d.rowptr = rowptr;
+        d.rcol = rcol; d.rval = rval; d.b = b; d.sense = sense; d.row_slack = row_slack; d.slack_row = slack_row;
+        d.c = c; d.lo = lo; d.hi = hi; d.unit_fixed = unit_fixed; d.z = z; d.r = r; d.ua = ua;
+        lp->colour = colour; lp->members = members; lp->heavy = heavy; lp->red = red; lp->flags = flags;
+        lp->temp = (char*)ws + temp_start;
+        lp->temp_bytes = total - temp_start;
+        *scan_buf = scan;
+        *cub_buf = cubp;
+        *cub_bytes = cb;
+    }
+    return total + 256;
+}
+
+size_t generic_workspace(int64_t m, int64_t n, int64_t nnz, bool has_val, bool, thetis_lp*, void*) {
+    return generic_layout(m, n, nnz, has_val, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+// --------------------------------------------------------------------------
+int recompute_r(thetis_lp* lp) {
+    if (lp->d.m > 0) k_recompute_r<<<grid_for(lp->d.m, T), T, 0, lp->stream>>>(lp->d);
+    return check_cuda(lp, "recompute_r");
+}
+int recompute_ua(thetis_lp* lp) {
+    if (lp->d.n_s > 0) k_recompute_ua<<<grid_for(lp->d.n_s, T), T, 0, lp->stream>>>(lp->d);
+    return check_cuda(lp, "recompute_ua");
+}
+
+static int copy_in(thetis_lp* lp, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return THETIS_OK;
+    CUDA_TRY(lp, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, lp->stream));
+    return THETIS_OK;
+}
+// device pointers are used in place, host inputs are staged into `buf`
+static const void* stage(thetis_lp* lp, const void* src, void* buf, size_t bytes, int* rc) {
+    *rc = THETIS_OK;
+    if (!src || bytes == 0 || is_device_ptr(src)) return src;
+    *rc = copy_in(lp, buf, src, bytes);
+    return buf;
+}
+
+static int read_flags(thetis_lp* lp, int32_t* h) {
+    CUDA_TRY(lp, cudaMemcpyAsync(h, lp->flags, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, lp->stream));
+    CUDA_TRY(lp, cudaStreamSynchronize(lp->stream));
+    return THETIS_OK;
+}
+
+static void fill_units(thetis_lp* lp) {
+    DevLP& d = lp->d;
+    d.N = d.n_s + d.n_ineq;
+    d.n_scalar = d.n_s - d.n_blocks * (d.n_blocks > 0 ? d.k : 0);
+    d.U = d.n_blocks + d.n_scalar + d.n_ineq;
+}
+
+int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t* src, const int32_t* dst,
+                const float* vertex_w, const float* edge_w, int k, const int32_t* terminals, int t_per_label) {
+    GraphTemps t{};
+    graph_layout(problem, n, E, k, lp, lp->ws, &t);
+    cudaStream_t s = lp->stream;
+    DevLP& d = lp->d;
+    const bool mwc = problem == THETIS_PROB_MWC;
+    int rc;
+    d.problem = problem;
+    d.obj_sense = problem == THETIS_PROB_MIS ? THETIS_MAX : THETIS_MIN;
+    d.c_sign = problem == THETIS_PROB_MIS ? -1.0f : 1.0f;
+    d.k = mwc ? k : 0;
+    d.n_vert = n;
+    CUDA_TRY(lp, cudaMemsetAsync(lp->flags, 0, 64 * sizeof(int32_t), s));
+    const int32_t* srcd = (const int32_t*)stage(lp, src, t.src_stage, (size_t)E * 4, &rc);
+    THETIS_TRY(rc);
+    const int32_t* dstd = (const int32_t*)stage(lp, dst, t.dst_stage, (size_t)E * 4, &rc);
+    THETIS_TRY(rc);
+    if (!mwc) THETIS_TRY(copy_in(lp, (void*)d.c, vertex_w, (size_t)n * 4));
+    if (mwc) THETIS_TRY(copy_in(lp, t.ew_in, edge_w, (size_t)E * 4));
+    if (mwc && t_per_label > 0) THETIS_TRY(copy_in(lp, t.terms, terminals, (size_t)k * t_per_label * 4));
+
+    // ---- K1: canonical keys u*n+v (u < v), sort, unique -> rows
+    int64_t m = 0;
+    if (E > 0) {
+        k_make_keys<<<grid_for(E, T), T, 0, s>>>(E, n, srcd, dstd, t.keys, mwc ? t.idx : nullptr, lp->flags);
+        const uint64_t sent = (uint64_t)n * (uint64_t)n;
+        const int end_bit = bits_for(sent);
+        size_t cb = t.cub_bytes;
+        cub::DoubleBuffer<uint64_t> dk(t.keys, t.keys2);
+        const uint64_t* uniq;
+        const int32_t* first_idx = nullptr;
+        if (mwc) {
+            cub::DoubleBuffer<int32_t> di(t.idx, t.idx2);
+            CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(t.cub, cb, dk, di, E, 0, end_bit, s));
+            cb = t.cub_bytes;
+            CUDA_TRY(lp, cub::DeviceSelect::UniqueByKey(t.cub, cb, dk.Current(), di.Current(), dk.Alternate(),
+                                                         di.Alternate(), t.nsel, E, s));
+            uniq = dk.Alternate();
+            first_idx = di.Alternate(); // stable sort: the first occurrence of each pair
+        } else {
+            CUDA_TRY(lp, cub::DeviceRadixSort::SortKeys(t.cub, cb, dk, E, 0, end_bit, s));
+            cb = t.cub_bytes;
+            CUDA_TRY(lp, cub::DeviceSelect::Unique(t.cub, cb, dk.Current(), dk.Alternate(), t.nsel, E, s));
+            uniq = dk.Alternate();
+        }
+        int64_t nsel = 0;
+        uint64_t last = 0;
+        CUDA_TRY(lp, cudaMemcpyAsync(&nsel, t.nsel, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        if (nsel > 0) {
+            CUDA_TRY(lp, cudaMemcpyAsync(&last, uniq + nsel - 1, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+        }
+        m = nsel - (nsel > 0 && last == sent ? 1 : 0);
+        int64_t rows = mwc ? 2 * (int64_t)k * m : m;
+        if (rows >= ((int64_t)1 << 31))
+            return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "too many rows (%lld) for int32 row indices", (long long)rows);
+        if (m > 0) k_decode_edges<<<grid_for(m, T), T, 0, s>>>(m, n, uniq, (int2*)d.edges);
+        if (mwc && m > 0) k_gather_ew<<<grid_for(m, T), T, 0, s>>>(m, first_idx, t.ew_in, (float*)d.ew);
+    }
+    d.m_edges = m;
+    THETIS_TRY(check_cuda(lp, "build: keys"));
+
+    // ---- incidence lists, ascending edge order per vertex: runs of u in row
+    // order, runs of v after a stable (v, e) sort
+    int64_t* iptr = mwc ? t.iptr : (int64_t*)d.colptr;
+    int32_t* inc = mwc ? t.inc : (int32_t*)d.rowidx;
+    if (n > 0) {
+        CUDA_TRY(lp, cudaMemsetAsync(t.us, 0, (size_t)n * 4, s));
+        CUDA_TRY(lp, cudaMemsetAsync(t.ue, 0, (size_t)n * 4, s));
+        CUDA_TRY(lp, cudaMemsetAsync(t.ls, 0, (size_t)n * 4, s));
+        CUDA_TRY(lp, cudaMemsetAsync(t.le, 0, (size_t)n * 4, s));
+    }
+    const int32_t* vsorted = nullptr;
+    const int32_t* esorted = nullptr;
+    if (m > 0) {
+        k_runs_u<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, t.ue);
+        k_vkeys<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.vkey, t.eval);
+        cub::DoubleBuffer<int32_t> dv(t.vkey, t.vkey2), de(t.eval, t.eval2);
+        size_t cb = t.cub_bytes;
+        CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(t.cub, cb, dv, de, m, 0, bits_for((uint64_t)n), s));
+        vsorted = dv.Current();
+        esorted = de.Current();
+        k_runs_key<<<grid_for(m, T), T, 0, s>>>(m, vsorted, t.ls, t.le);
+    }
+    k_degrees<<<grid_for(n + 1, T), T, 0, s>>>(n, t.us, t.ue, t.ls, t.le, t.deg);
+    {
+        size_t cb = t.cub_bytes;
+        CUDA_TRY(lp, cub::DeviceScan::ExclusiveSum(t.cub, cb, t.deg, iptr, n + 1, s));
+    }
+    if (m > 0) {
+        k_fill_lower<<<grid_for(m, T), T, 0, s>>>(m, vsorted, esorted, t.ls, iptr, inc);
+        k_fill_upper<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, t.ls, t.le, iptr, inc);
+    }
+    THETIS_TRY(check_cuda(lp, "build: incidence"));
+
+    unsigned long long* maxdeg = (unsigned long long*)(lp->flags + 16);
+    if (!mwc) {
+        // ---- K2 VC / MIS: the incidence lists are the CSC (all coefficients +1)
+        d.m = m;
+        d.n_s = n;
+        d.nnz_s = 2 * m;
+        d.n_ineq = m;
+        d.n_blocks = 0;
+        if (n > 0) k_max_deg<<<grid_for(n, T), T, 0, s>>>(n, d.colptr, maxdeg);
+        CUDA_TRY(lp, cudaMemsetAsync(d.z, 0, (size_t)(n + m) * 4, s));
+    } else {
+        // ---- K2 MWC: expand the incidence into the k label columns + edge-label columns
+        const int64_t nk = n * k;
+        d.m = 2 * (int64_t)k * m;
+        d.n_s = nk + m * k;
+        d.nnz_s = 6 * (int64_t)k * m;
+        d.n_ineq = d.m;
+        d.n_blocks = n;
+        k_mwc_colptr<<<grid_for(d.n_s + 1, T), T, 0, s>>>(n, m, k, iptr, (int64_t*)d.colptr);
+        if (n > 0) k_mwc_fill_vertex<<<grid_for(n, 128), 128, 0, s>>>(n, k, iptr, inc, d.edges, d.colptr,
+                                                                       (int32_t*)d.rowidx);
+        CUDA_TRY(lp, cudaMemsetAsync((void*)d.c, 0, (size_t)nk * 4, s));
+        if (m > 0) k_mwc_fill_edge<<<grid_for(m * k, T), T, 0, s>>>(m, k, 4 * (int64_t)k * m, (int32_t*)d.rowidx,
+                                                                     d.ew, (float*)d.c, nk);
+        CUDA_TRY(lp, cudaMemsetAsync((void*)d.term_label, 0xFF, (size_t)n * 4, s));
+        if (t_per_label > 0)
+            k_mwc_terminals<<<grid_for((int64_t)k * t_per_label, T), T, 0, s>>>(n, k, t_per_label, t.terms,
+                                                                                (int32_t*)d.term_label, lp->flags);
+        CUDA_TRY(lp, cudaMemsetAsync(d.z, 0, (size_t)(d.n_s + d.m) * 4, s));
+        const int64_t S = n + m * k;
+        if (S > 0) k_mwc_init<<<grid_for(S, T), T, 0, s>>>(n, k, d.term_label, d.z, (uint8_t*)d.unit_fixed, S);
+        if (d.n_s > 0) k_max_deg<<<grid_for(d.n_s, T), T, 0, s>>>(d.n_s, d.colptr, maxdeg);
+    }
+    fill_units(lp);
+    CUDA_TRY(lp, cudaMemsetAsync(d.ua, 0, (size_t)(d.n_s > 0 ? d.n_s : 1) * 4, s));
+    THETIS_TRY(recompute_r(lp));
+    int32_t h[8];
+    unsigned long long md = 0;
+    CUDA_TRY(lp, cudaMemcpyAsync(&md, maxdeg, 8, cudaMemcpyDeviceToHost, s));
+    THETIS_TRY(read_flags(lp, h));
+    if (h[FLAG_BAD_INPUT]) return set_error(lp, THETIS_ERR_INVALID_ARG, "vertex id out of range [0, n)");
+    if (h[FLAG_DUP_TERMINAL]) return set_error(lp, THETIS_ERR_INVALID_ARG, "a vertex is a terminal twice");
+    lp->maxnorm2 = (double)md;
+    if (d.n_ineq > 0 && lp->maxnorm2 < 1.0) lp->maxnorm2 = 1.0; // slack columns
+    return THETIS_OK;
+}
+
+int build_generic(thetis_lp* lp, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                  const float* val, const int64_t* rowptr, const int32_t* rcol, const float* rval, const float* b,
+                  const float* c, const int8_t* sense, const float* lo, const float* hi, int obj_sense, int block_k,
+                  int64_t n_blocks) {
+    int32_t* scan = nullptr;
+    void* cubp = nullptr;
+    size_t cb = 0;
+    generic_layout(m, n, nnz, val != nullptr, lp, lp->ws, &scan, &cubp, &cb);
+    cudaStream_t s = lp->stream;
+    DevLP& d = lp->d;
+    d.problem = THETIS_PROB_GENERIC;
+    d.obj_sense = obj_sense;
+    d.c_sign = obj_sense == THETIS_MAX ? -1.0f : 1.0f;
+    d.k = block_k;
+    d.m = m;
+    d.n_s = n;
+    d.nnz_s = nnz;
+    d.n_blocks = n_blocks;
+    d.n_vert = 0;
+    d.m_edges = 0;
+    if (!lo) d.lo = nullptr;
+    if (!hi) d.hi = nullptr;
+    CUDA_TRY(lp, cudaMemsetAsync(lp->flags, 0, 64 * sizeof(int32_t), s));
+    THETIS_TRY(copy_in(lp, (void*)d.colptr, colptr, (size_t)(n + 1) * 8));
+    THETIS_TRY(copy_in(lp, (void*)d.rowidx, rowidx, (size_t)nnz * 4));
+    if (val) THETIS_TRY(copy_in(lp, (void*)d.val, val, (size_t)nnz * 4));
+    THETIS_TRY(copy_in(lp, (void*)d.rowptr, rowptr, (size_t)(m + 1) * 8));
+    THETIS_TRY(copy_in(lp, (void*)d.rcol, rcol, (size_t)nnz * 4));
+    if (val) THETIS_TRY(copy_in(lp, (void*)d.rval, rval, (size_t)nnz * 4));
+    THETIS_TRY(copy_in(lp, (void*)d.b, b, (size_t)m * 4));
+    THETIS_TRY(copy_in(lp, (void*)d.c, c, (size_t)n * 4));
+    if (sense) THETIS_TRY(copy_in(lp, (void*)d.sense, sense, (size_t)m));
+    else if (m > 0) CUDA_TRY(lp, cudaMemsetAsync((void*)d.sense, 0, (size_t)m, s));
+    if (lo) THETIS_TRY(copy_in(lp, (void*)d.lo, lo, (size_t)n * 4));
+    if (hi) THETIS_TRY(copy_in(lp, (void*)d.hi, hi, (size_t)n * 4));
+    // validation: CSC and CSR well formed, same entry set (fingerprint)
+    unsigned long long* fp = (unsigned long long*)(lp->flags + 16);
+    CUDA_TRY(lp, cudaMemsetAsync(fp, 0, 32, s));
+    if (n > 0) {
+        k_check_csc<<<grid_for(n, T), T, 0, s>>>(n, m, nnz, d.colptr, d.rowidx, lp->flags, FLAG_BAD_CSC);
+        k_fp_csc<<<grid_for(n, T), T, 0, s>>>(n, d.colptr, d.rowidx, d.val, fp);
+    }
+    if (m > 0) {
+        k_check_csc<<<grid_for(m, T), T, 0, s>>>(m, n, nnz, d.rowptr, d.rcol, lp->flags, FLAG_BAD_CSR);
+        k_fp_csr<<<grid_for(m, T), T, 0, s>>>(m, d.rowptr, d.rcol, d.rval, fp + 1);
+    }
+    // slack columns in row order (App. C)
+    int64_t n_ineq = 0;
+    if (m > 0) {
+        k_slack_flags<<<grid_for(m + 1, T), T, 0, s>>>(m, d.sense, scan, lp->flags);
+        size_t c2 = cb;
+        CUDA_TRY(lp, cub::DeviceScan::ExclusiveSum(cubp, c2, scan, scan + (m + 1), m + 1, s));
+        k_slack_maps<<<grid_for(m, T), T, 0, s>>>(m, n, d.sense, scan + (m + 1), (int64_t*)d.row_slack,
+                                                  (int32_t*)d.slack_row);
+        int32_t ni = 0;
+        CUDA_TRY(lp, cudaMemcpyAsync(&ni, scan + (m + 1) + m, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        n_ineq = ni;
+    }
+    d.n_ineq = n_ineq;
+    fill_units(lp);
+    unsigned long long* mx = fp + 2;
+    if (n > 0) k_colnorm2<<<grid_for(n, T), T, 0, s>>>(n, d.colptr, d.val, (double*)d.colnorm2, mx);
+    const int64_t S = d.n_blocks + d.n_scalar;
+    CUDA_TRY(lp, cudaMemsetAsync(d.z, 0, (size_t)(d.N > 0 ? d.N : 1) * 4, s));
+    if (S > 0) k_generic_init<<<grid_for(S, T), T, 0, s>>>(n, n_blocks, block_k, d.lo, d.hi, d.z,
+                                                         (uint8_t*)d.unit_fixed, lp->flags);
+    CUDA_TRY(lp, cudaMemsetAsync(d.ua, 0, (size_t)(n > 0 ? n : 1) * 4, s));
+    THETIS_TRY(recompute_r(lp));
+    int32_t h[8];
+    unsigned long long hfp[3] = {0, 0, 0};
+    CUDA_TRY(lp, cudaMemcpyAsync(hfp, fp, 24, cudaMemcpyDeviceToHost, s));
+    THETIS_TRY(read_flags(lp, h));
+    if (h[FLAG_BAD_CSC]) return set_error(lp, THETIS_ERR_INVALID_ARG, "malformed CSC (pointers or row indices)");
+    if (h[FLAG_BAD_CSR]) return set_error(lp, THETIS_ERR_INVALID_ARG, "malformed CSR (pointers or column indices)");
+    if (h[FLAG_BAD_INPUT]) return set_error(lp, THETIS_ERR_INVALID_ARG, "row sense not in {EQ, GE, LE}");
+    if (h[FLAG_BAD_BOUNDS]) return set_error(lp, THETIS_ERR_INVALID_ARG, "lo > hi");
+    if (hfp[0] != hfp[1]) return set_error(lp, THETIS_ERR_INVALID_ARG, "CSC and CSR hold different entries");
+    double mxd;
+    memcpy(&mxd, &hfp[2], 8);
+    lp->maxnorm2 = mxd;
+    if (d.n_ineq > 0 && lp->maxnorm2 < 1.0) lp->maxnorm2 = 1.0;
+    return THETIS_OK;
+}
+
+}  // namespace thetis
