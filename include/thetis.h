@@ -67,7 +67,8 @@ typedef enum {
 enum { THETIS_EQ = 0, THETIS_GE = 1, THETIS_LE = 2 };          /* row sense */
 enum { THETIS_MIN = 0, THETIS_MAX = 1 };                       /* objective sense */
 enum { THETIS_PROB_GENERIC = 0, THETIS_PROB_VC = 1, THETIS_PROB_MIS = 2, THETIS_PROB_MWC = 3 };
-enum { THETIS_MODE_DETERMINISTIC = 0, THETIS_MODE_ASYNC = 1 };
+enum { THETIS_MODE_DETERMINISTIC = 0, THETIS_MODE_ASYNC = 1,
+       THETIS_MODE_ASYNC_SERIAL = 2 /* diagnostic: the async kernel with one tile in flight */ };
 enum { THETIS_STEP_LMAX = 0, /* Alg. 1: 1/L_max, Eq. 7 */
        THETIS_STEP_LJ = 1    /* 1/L_j per unit: extension, not the paper's (R-4) */ };
 enum { THETIS_ROUND_VC_HALF = 1,   /* Lemma-1 threshold (1-eps)/2 + fix-up */
@@ -176,6 +177,8 @@ THETIS_API int thetis_get_r(const thetis_lp* lp, float* dst, int64_t count);
  *  THETIS_MODE_ASYNC: tiles of 32 units in a per-epoch keyed permutation
  *    (R-6), processed concurrently Hogwild-style with atomic
  *    residual updates.
+ *  THETIS_MODE_ASYNC_SERIAL: the async kernel with a single tile in flight,
+ *    i.e. the tile-synchronous replay of the permutation (diagnostic / tests).
  * seed keys the colouring (det) or the permutations (async).  stats (host)
  * may be NULL; if given, the call synchronises and fills it. */
 THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,

@@ -582,37 +582,45 @@ static REAL unit_invL(const ref_lp* lp, const step_ctx* s, int64_t first, int64_
 }
 
 /* Alg. 1 line 4 on unit u, generalised to the box [lo, hi] (R-2) and to
- * k-blocks with simplex projection (App. E).  Returns the nnz touched. */
-static int64_t step_unit(ref_lp* lp, const step_ctx* s, int64_t u) {
+ * k-blocks with simplex projection (App. E): the new values of the unit's
+ * columns, from the current z and r (nothing is modified). */
+static void unit_new_values(const ref_lp* lp, const step_ctx* s, int64_t u, REAL* out) {
     int64_t f, c;
     unit_cols(lp, u, &f, &c);
-    if (unit_fixed(lp, u)) return 0;
     REAL invL = unit_invL(lp, s, f, c);
     if (u < lp->n_blocks) {
-        REAL y[64], x[64];
+        REAL y[64];
         for (int64_t l = 0; l < c; l++) {
             REAL g = grad_col(lp, s->beta, f + l);
             y[l] = lp->z[f + l] - g * invL;
         }
-        project_simplex(y, (int)c, x);
-        int64_t nz = 0;
-        for (int64_t l = 0; l < c; l++) {
-            REAL d = x[l] - lp->z[f + l];
-            col_axpy(lp, f + l, d);
-            lp->z[f + l] = x[l];
-            nz += col_nnz(lp, f + l);
-        }
-        return nz;
+        project_simplex(y, (int)c, out);
+        return;
     }
     REAL g = grad_col(lp, s->beta, f);
     REAL t = lp->z[f] - g * invL;
     REAL lo = col_lo(lp, f), hi = col_hi(lp, f);
     REAL zn = t < lo ? lo : t;
-    zn = zn > hi ? hi : zn;
-    REAL d = zn - lp->z[f];
-    col_axpy(lp, f, d);
-    lp->z[f] = zn;
-    return col_nnz(lp, f);
+    out[0] = zn > hi ? hi : zn;
+}
+/* z_j <- new value, r += a_j (new - old) for the unit's columns; returns nnz touched */
+static int64_t apply_unit(ref_lp* lp, int64_t u, const REAL* nv) {
+    int64_t f, c, nz = 0;
+    unit_cols(lp, u, &f, &c);
+    for (int64_t l = 0; l < c; l++) {
+        REAL d = nv[l] - lp->z[f + l];
+        col_axpy(lp, f + l, d);
+        lp->z[f + l] = nv[l];
+        nz += col_nnz(lp, f + l);
+    }
+    return nz;
+}
+/* one step of Alg. 1 on unit u; returns the nnz touched (0 if the unit is fixed) */
+static int64_t step_unit(ref_lp* lp, const step_ctx* s, int64_t u) {
+    if (unit_fixed(lp, u)) return 0;
+    REAL nv[64];
+    unit_new_values(lp, s, u, nv);
+    return apply_unit(lp, u, nv);
 }
 
 int thetis_ref_step_unit(ref_lp* lp, float beta, int64_t u, int step_rule) {
@@ -723,9 +731,27 @@ void thetis_ref_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t
     }
 }
 
+/* Tile-synchronous replay (test reference for the kernel's semantics at one
+ * tile in flight): every unit of the tile takes its step from the state at the
+ * tile's start, then all changes are applied in unit order. */
+static int64_t step_tile_sync(ref_lp* lp, const step_ctx* s, int64_t u0, int64_t u1, int64_t* updates,
+                              REAL* nv) {
+    int64_t nz = 0, kk = lp->block_k > 0 ? lp->block_k : 1;
+    for (int64_t u = u0; u < u1; u++)
+        if (!unit_fixed(lp, u)) unit_new_values(lp, s, u, nv + (u - u0) * kk);
+    for (int64_t u = u0; u < u1; u++) {
+        if (unit_fixed(lp, u)) continue;
+        int64_t f, c;
+        unit_cols(lp, u, &f, &c);
+        nz += apply_unit(lp, u, nv + (u - u0) * kk);
+        *updates += c;
+    }
+    return nz;
+}
+
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                      ref_stats* st) {
-    if (!(beta > 0) || epochs < 0 || mode < 0 || mode > 2 || step_rule < 0 || step_rule > 1)
+    if (!(beta > 0) || epochs < 0 || mode < 0 || mode > 3 || step_rule < 0 || step_rule > 1)
         return REF_INVALID_ARG;
     step_ctx s = make_ctx(lp, beta, step_rule);
     if (lp->ubar) recompute_ua(lp);
@@ -743,7 +769,7 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                 if (colour[u] == cl) order[n_order++] = u;
     }
     int64_t n_tiles = (lp->U + 31) / 32;
-    int64_t* perm = mode == MODE_ASYNC ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
+    int64_t* perm = (mode == MODE_ASYNC || mode == 3) ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
     for (int e = 0; e < epochs; e++) {
         if (mode == MODE_DET) {
             for (int64_t p = 0; p < n_order; p++) {
@@ -762,6 +788,13 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                     nnz += step_unit(lp, &s, u);
                     updates += c;
                 }
+        } else if (mode == 3) {
+            REAL nv[32 * 64];
+            thetis_ref_tile_perm(n_tiles, seed, e, perm);
+            for (int64_t t = 0; t < n_tiles; t++) {
+                int64_t u1 = perm[t] * 32 + 32 < lp->U ? perm[t] * 32 + 32 : lp->U;
+                nnz += step_tile_sync(lp, &s, perm[t] * 32, u1, &updates, nv);
+            }
         } else {
             for (int64_t u = 0; u < lp->U; u++) {
                 if (unit_fixed(lp, u)) continue;

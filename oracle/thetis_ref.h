@@ -92,8 +92,13 @@ int thetis_ref_step_unit(ref_lp* lp, float beta, int64_t u, int step_rule);
 /* partial derivative of f_beta w.r.t. column j at the current point */
 double thetis_ref_grad(const ref_lp* lp, float beta, int64_t j);
 
-/* mode 0 = deterministic coloured sweep, 1 = async reference trajectory
- * (sequential replay of the tile permutation), 2 = plain cyclic sweep. */
+/* mode 0 = deterministic coloured sweep (R-5);
+ * mode 1 = unit-sequential replay of the tile permutation (Alg. 1 one
+ *          coordinate at a time, in the async order);
+ * mode 2 = plain cyclic sweep;
+ * mode 3 = the async reference trajectory (R-6): tiles in permutation order,
+ *          each tile one synchronous step of its 32 units (every unit steps
+ *          from the state at the tile's start, then all are applied). */
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                      int step_rule, ref_stats* st);
 int thetis_ref_objective(const ref_lp* lp, float beta, ref_objective* out);

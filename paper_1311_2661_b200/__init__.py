@@ -33,7 +33,7 @@ THETIS_ERR_ROUND_PRECONDITION = -6
 THETIS_EQ, THETIS_GE, THETIS_LE = 0, 1, 2
 THETIS_MIN, THETIS_MAX = 0, 1
 THETIS_PROB_GENERIC, THETIS_PROB_VC, THETIS_PROB_MIS, THETIS_PROB_MWC = 0, 1, 2, 3
-THETIS_MODE_DETERMINISTIC, THETIS_MODE_ASYNC = 0, 1
+THETIS_MODE_DETERMINISTIC, THETIS_MODE_ASYNC, THETIS_MODE_ASYNC_SERIAL = 0, 1, 2
 THETIS_STEP_LMAX, THETIS_STEP_LJ = 0, 1
 THETIS_ROUND_VC_HALF, THETIS_ROUND_VC_FIXUP, THETIS_ROUND_MIS_GREEDY, THETIS_ROUND_MWC_CKR = 1, 2, 3, 4
 THETIS_MAX_EPOCH_TIMES = 64
@@ -152,8 +152,11 @@ class LP:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            thetis_free(h)
+        if h and _L is not None:
+            try:
+                _L.thetis_free(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     @staticmethod

@@ -220,7 +220,7 @@ THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uin
                             thetis_solve_stats* stats) {
     if (!lp) return THETIS_ERR_INVALID_ARG;
     if (!(beta > 0.0f) || !isfinite(beta) || epochs < 0 ||
-        (mode != THETIS_MODE_DETERMINISTIC && mode != THETIS_MODE_ASYNC) ||
+        (mode != THETIS_MODE_DETERMINISTIC && mode != THETIS_MODE_ASYNC && mode != THETIS_MODE_ASYNC_SERIAL) ||
         (step_rule != THETIS_STEP_LMAX && step_rule != THETIS_STEP_LJ))
         return set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments to thetis_solve");
     if (lp->anchors) THETIS_TRY(recompute_ua(lp));

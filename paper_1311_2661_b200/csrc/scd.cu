@@ -15,11 +15,14 @@
 // fp32 build of the oracle.
 //
 // Async mode (R-6): tiles of 32 consecutive units in a per-epoch keyed
-// permutation; a warp owns a tile, gathers r with L2 loads (ld.global.cg; stale
-// values allowed: Hogwild), scatters with red.global.add.f32.  Scalar-column
-// tiles are processed cooperatively: the tile's nonzeros are one contiguous
-// CSC range, read coalesced 32 at a time; tiles with more than kHeavy nonzeros go
-// to a CTA-per-tile kernel on a concurrent stream.
+// permutation; one persistent kernel, a warp per tile, tile-synchronous inside
+// the tile (all gathers, then all scatters), Hogwild across tiles: r is read
+// with L2 loads (ld.global.cg; stale values allowed) and written with
+// red.global.add.f32, so no update is lost.  Scalar-column tiles are processed
+// cooperatively: the tile's nonzeros are one contiguous CSC range, read
+// coalesced 32 at a time; a tile with more than kHeavy nonzeros is finished by
+// its whole CTA at its place in the sequence.  The grid bounds the number of
+// tiles in flight to ~n_tiles / kAsyncDepth (bounded staleness).
 #include "thetis_internal.cuh"
 
 namespace thetis {
@@ -27,7 +30,6 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int64_t kHeavy = 2048;    // async: scalar nnz per tile above which a CTA takes it
-constexpr int kHeavyThreads = 512;
 constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the warp path
 
 struct StepParams {
@@ -246,11 +248,7 @@ __global__ void __launch_bounds__(256) k_det_slacks(DevLP L, StepParams P) {
 }
 
 // ------------------------------------------------------------ async
-struct TileRanges {
-    int64_t u0, nb_end, sc_end, U;
-};
-
-// scalar sub-range [a, b) of the tile's lanes and their columns
+// scalar sub-range [a, b) of the tile's lanes
 __device__ __forceinline__ void scalar_lanes(const DevLP& L, int64_t u0, int& a, int& b) {
     const int64_t s0 = L.n_blocks, s1 = L.n_blocks + L.n_scalar;
     int64_t lo = u0 > s0 ? u0 : s0, hi = u0 + 32 < s1 ? u0 + 32 : s1;
@@ -259,135 +257,182 @@ __device__ __forceinline__ void scalar_lanes(const DevLP& L, int64_t u0, int& a,
     b = (int)(hi - u0);
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async_tiles(DevLP L, StepParams P, PermKeys K,
-                                                                     int64_t n_tiles) {
-    __shared__ float acc_s[kWarpsPerBlock][32];
-    __shared__ float d_s[kWarpsPerBlock][32];
-    __shared__ int32_t head_s[kWarpsPerBlock][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t t_idx = blockIdx.x * (int64_t)kWarpsPerBlock + w;
-    if (t_idx >= n_tiles) return;
-    const int64_t tile = (int64_t)tile_perm((uint64_t)t_idx, K);
-    const int64_t u0 = tile * 32;
-    const int64_t u = u0 + lane;
-    // blocks and slacks: one lane each
-    if (u < L.U) {
-        if (u < L.n_blocks) {
-            if (!(L.unit_fixed && L.unit_fixed[u])) update_block_seq<true>(L, P, u);
-        } else if (u >= L.n_blocks + L.n_scalar) {
-            update_slack<true>(L, P, u - L.n_blocks - L.n_scalar);
+// new values of a k-block from the current (possibly stale) residual
+__device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P, int64_t u, float* x) {
+    const int k = L.k;
+    const int64_t f = u * k;
+    float y[kMaxK];
+    double mx = 0.0;
+    if (P.rule == THETIS_STEP_LJ)
+        for (int l = 0; l < k; l++) {
+            double q = col_norm2(L, f + l);
+            mx = q > mx ? q : mx;
         }
+    const float invL = unit_invL(P, mx);
+    for (int l = 0; l < k; l++) {
+        int64_t j = f + l;
+        float D = col_dot_seq<true>(L, j);
+        float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
+        y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
     }
-    // scalar columns: the tile's nonzeros are one contiguous CSC range
+    project_simplex(y, k, x);
+}
+
+struct WarpSmem {
+    float acc[32];
+    float d[32];
+    int32_t head[32];
+};
+
+// column (lane index) of the nonzero at position base + lane: the segment heads
+// falling in the chunk, max-scanned, carried over from the previous chunk
+__device__ __forceinline__ int chunk_col(int lane, int ncols, int64_t cp, int64_t base, int64_t end, int32_t* head,
+                                         int& carry) {
+    head[lane] = -1;
+    __syncwarp();
+    if (lane < ncols && cp >= base && cp < base + 32 && cp < end) atomicMax(&head[(int)(cp - base)], lane);
+    __syncwarp();
+    int col = head[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int x = __shfl_up_sync(0xffffffffu, col, o);
+        if (lane >= o) col = x > col ? x : col;
+    }
+    col = col > carry ? col : carry;
+    carry = __shfl_sync(0xffffffffu, col, 31);
+    __syncwarp();
+    return col;
+}
+
+// One tile, one warp, tile-synchronous: every unit of the tile gathers from the
+// residual as it is when the tile starts (stale w.r.t. other tiles in flight),
+// then all units scatter.  Scalar columns are processed cooperatively over the
+// tile's contiguous CSC range.  Returns true (warp-uniform) when the scalar range
+// has more than heavy_limit nonzeros: the whole CTA then finishes it.
+__device__ __forceinline__ bool async_tile_warp(const DevLP& L, const StepParams& P, int64_t tile, int lane,
+                                                WarpSmem& sm, int64_t heavy_limit) {
+    const int64_t u0 = tile * 32, u = u0 + lane;
+    const bool is_block = u < L.U && u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
+    const bool is_slack = u < L.U && u >= L.n_blocks + L.n_scalar;
+    float xb[kMaxK];
+    if (is_block) block_values(L, P, u, xb);
+    float ds = 0.0f, sig = 0.0f;
+    int64_t srow = 0;
+    if (is_slack) {
+        const int64_t q = u - L.n_blocks - L.n_scalar, j = L.n_s + q;
+        srow = slack_row_of(L, q);
+        sig = row_sigma(L, srow);
+        float rv = ld_cg(L.r + srow);
+        float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
+        float ua = 0.0f;
+        if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[srow] : L.ubar[srow]);
+        float z = L.z[j];
+        float g = grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
+        float t = __fsub_rn(z, __fmul_rn(g, unit_invL(P, 1.0)));
+        float zn = t < 0.0f ? 0.0f : t;
+        ds = __fsub_rn(zn, z);
+        L.z[j] = zn;
+    }
+    // scalar columns
     int a, b;
     scalar_lanes(L, u0, a, b);
-    if (a >= b) return;
-    const int64_t j0 = L.n_blocks * L.k + (u0 + a - L.n_blocks);
     const int ncols = b - a;
-    // lane i < ncols holds the start of column j0 + i; lane ncols holds the end
-    const int64_t cp = lane <= ncols ? L.colptr[j0 + lane] : 0;
-    const int64_t beg = __shfl_sync(0xffffffffu, cp, 0);
-    const int64_t end = __shfl_sync(0xffffffffu, cp, ncols);
-    if (end - beg > kHeavy) return; // heavy tile: k_async_heavy
-    acc_s[w][lane] = 0.0f;
-    __syncwarp();
-    // pass 1: D_i = a_i^T r, segmented by column (head of each segment via
-    // a max-scan over the column starts falling in the chunk)
-    int carry = 0; // column owning the first nonzero of the chunk
-    for (int64_t base = beg; base < end; base += 32) {
-        head_s[w][lane] = -1;
-        __syncwarp();
-        if (lane < ncols && cp >= base && cp < base + 32 && cp < end) atomicMax(&head_s[w][(int)(cp - base)], lane);
-        __syncwarp();
-        int col = head_s[w][lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            int x = __shfl_up_sync(0xffffffffu, col, o);
-            if (lane >= o) col = x > col ? x : col;
-        }
-        col = col > carry ? col : carry;
-        carry = __shfl_sync(0xffffffffu, col, 31);
-        const int64_t t = base + lane;
-        if (t < end) {
-            int64_t row;
-            float av;
-            entry(L, t, row, av);
-            float rv = ld_cg(L.r + row);
-            atomicAdd(&acc_s[w][col], L.val ? av * rv : (av < 0.0f ? -rv : rv));
-        }
-        __syncwarp();
+    bool heavy = false, coop = false;
+    int64_t j0 = 0, cp = 0, beg = 0, end = 0;
+    if (ncols > 0) {
+        j0 = L.n_blocks * L.k + (u0 + a - L.n_blocks);
+        cp = lane < ncols ? L.colptr[j0 + lane] : 0;
+        beg = __shfl_sync(0xffffffffu, cp, 0);
+        end = L.colptr[j0 + ncols];
+        heavy = end - beg > heavy_limit;
+        coop = !heavy;
     }
-    // the coordinate step, one lane per column
-    float d = 0.0f;
-    if (lane < ncols) {
-        const int64_t j = j0 + lane;
-        const bool fixed = L.unit_fixed && L.unit_fixed[u0 + a + lane];
-        if (!fixed) {
+    unsigned moved = 0;
+    if (coop) {
+        sm.acc[lane] = 0.0f;
+        __syncwarp();
+        int carry = 0;
+        for (int64_t base = beg; base < end; base += 32) {
+            const int col = chunk_col(lane, ncols, cp, base, end, sm.head, carry);
+            const int64_t t = base + lane;
+            if (t < end) {
+                int64_t row;
+                float av;
+                entry(L, t, row, av);
+                float rv = ld_cg(L.r + row);
+                atomicAdd(&sm.acc[col], L.val ? av * rv : (av < 0.0f ? -rv : rv));
+            }
+        }
+        __syncwarp();
+        float d = 0.0f;
+        if (lane < ncols && !(L.unit_fixed && L.unit_fixed[u0 + a + lane])) {
+            const int64_t j = j0 + lane;
             float z = L.z[j];
-            float g = grad_from(c_int(L, j), ua_of(L, j), acc_s[w][lane], z, zbar_of(L, j), P.beta);
+            float g = grad_from(c_int(L, j), ua_of(L, j), sm.acc[lane], z, zbar_of(L, j), P.beta);
             float invL = unit_invL(P, col_norm2(L, j));
             float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
             d = __fsub_rn(zn, z);
             L.z[j] = zn;
         }
+        sm.d[lane] = d;
+        moved = __ballot_sync(0xffffffffu, d != 0.0f);
     }
-    d_s[w][lane] = d;
-    const unsigned moved = __ballot_sync(0xffffffffu, d != 0.0f);
     __syncwarp();
-    if (!moved) return;
-    // pass 2: r += a_j d_j
-    carry = 0;
-    for (int64_t base = beg; base < end; base += 32) {
-        head_s[w][lane] = -1;
-        __syncwarp();
-        if (lane < ncols && cp >= base && cp < base + 32 && cp < end) atomicMax(&head_s[w][(int)(cp - base)], lane);
-        __syncwarp();
-        int col = head_s[w][lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            int x = __shfl_up_sync(0xffffffffu, col, o);
-            if (lane >= o) col = x > col ? x : col;
+    // scatter phase
+    if (is_block) {
+        for (int l = 0; l < L.k; l++) {
+            const int64_t j = u * L.k + l;
+            float d = __fsub_rn(xb[l], L.z[j]);
+            col_scatter<true>(L, j, d);
+            L.z[j] = xb[l];
         }
-        col = col > carry ? col : carry;
-        carry = __shfl_sync(0xffffffffu, col, 31);
-        const int64_t t = base + lane;
-        const float dc = d_s[w][col];
-        if (t < end && dc != 0.0f) {
-            int64_t row;
-            float av;
-            entry(L, t, row, av);
-            red_add(L.r + row, L.val ? av * dc : (av < 0.0f ? -dc : dc));
-        }
-        __syncwarp();
     }
+    if (is_slack && ds != 0.0f) red_add(L.r + srow, sig < 0.0f ? -ds : ds);
+    if (moved) {
+        int carry = 0;
+        for (int64_t base = beg; base < end; base += 32) {
+            const int col = chunk_col(lane, ncols, cp, base, end, sm.head, carry);
+            const int64_t t = base + lane;
+            const float dc = sm.d[col];
+            if (t < end && dc != 0.0f) {
+                int64_t row;
+                float av;
+                entry(L, t, row, av);
+                red_add(L.r + row, L.val ? av * dc : (av < 0.0f ? -dc : dc));
+            }
+        }
+    }
+    return heavy;
 }
 
-// heavy scalar tiles: one CTA per tile
-__global__ void __launch_bounds__(kHeavyThreads) k_async_heavy(DevLP L, StepParams P, const int32_t* __restrict__ heavy,
-                                                               int64_t n_heavy) {
-    __shared__ float acc_s[32];
-    __shared__ float d_s[32];
-    __shared__ int64_t cp_s[33];
-    const int64_t h = blockIdx.x;
-    if (h >= n_heavy) return;
-    const int64_t u0 = (int64_t)heavy[h] * 32;
+struct CtaSmem {
+    float acc[32];
+    float d[32];
+    int64_t cp[33];
+};
+
+// the scalar range of a heavy tile, by the whole CTA (all threads call this)
+__device__ __forceinline__ void async_tile_cta(const DevLP& L, const StepParams& P, int64_t tile, CtaSmem& sm) {
+    const int64_t u0 = tile * 32;
     int a, b;
     scalar_lanes(L, u0, a, b);
     const int64_t j0 = L.n_blocks * L.k + (u0 + a - L.n_blocks);
     const int ncols = b - a;
-    if (threadIdx.x <= (unsigned)ncols) cp_s[threadIdx.x] = L.colptr[j0 + threadIdx.x];
-    if (threadIdx.x < 32) acc_s[threadIdx.x] = 0.0f;
+    if (threadIdx.x <= (unsigned)ncols) sm.cp[threadIdx.x] = L.colptr[j0 + threadIdx.x];
+    if (threadIdx.x < 32) sm.acc[threadIdx.x] = 0.0f;
     __syncthreads();
-    const int64_t beg = cp_s[0], end = cp_s[ncols];
+    const int64_t beg = sm.cp[0], end = sm.cp[ncols];
     for (int64_t t = beg + threadIdx.x; t < end; t += blockDim.x) {
         int lo = 0, hi = ncols - 1; // last column with start <= t
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
-            if (cp_s[mid] <= t) lo = mid; else hi = mid - 1;
+            if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
         }
         int64_t row;
         float av;
         entry(L, t, row, av);
         float rv = ld_cg(L.r + row);
-        atomicAdd(&acc_s[lo], L.val ? av * rv : (av < 0.0f ? -rv : rv));
+        atomicAdd(&sm.acc[lo], L.val ? av * rv : (av < 0.0f ? -rv : rv));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -396,38 +441,62 @@ __global__ void __launch_bounds__(kHeavyThreads) k_async_heavy(DevLP L, StepPara
         if (lane < ncols && !(L.unit_fixed && L.unit_fixed[u0 + a + lane])) {
             const int64_t j = j0 + lane;
             float z = L.z[j];
-            float g = grad_from(c_int(L, j), ua_of(L, j), acc_s[lane], z, zbar_of(L, j), P.beta);
+            float g = grad_from(c_int(L, j), ua_of(L, j), sm.acc[lane], z, zbar_of(L, j), P.beta);
             float invL = unit_invL(P, col_norm2(L, j));
             float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
             d = __fsub_rn(zn, z);
             L.z[j] = zn;
         }
-        d_s[lane] = d;
+        sm.d[lane] = d;
     }
     __syncthreads();
     for (int64_t t = beg + threadIdx.x; t < end; t += blockDim.x) {
         int lo = 0, hi = ncols - 1;
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
-            if (cp_s[mid] <= t) lo = mid; else hi = mid - 1;
+            if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
         }
-        float dc = d_s[lo];
+        float dc = sm.d[lo];
         if (dc == 0.0f) continue;
         int64_t row;
         float av;
         entry(L, t, row, av);
         red_add(L.r + row, L.val ? av * dc : (av < 0.0f ? -dc : dc));
     }
+    __syncthreads();
 }
 
-__global__ void k_find_heavy(DevLP L, int64_t n_tiles, int32_t* heavy, unsigned long long* count) {
-    for (int64_t tile = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tile < n_tiles;
-         tile += (int64_t)gridDim.x * blockDim.x) {
-        int a, b;
-        scalar_lanes(L, tile * 32, a, b);
-        if (a >= b) continue;
-        int64_t j0 = L.n_blocks * L.k + (tile * 32 + a - L.n_blocks);
-        if (L.colptr[j0 + (b - a)] - L.colptr[j0] > kHeavy) heavy[atomicAdd(count, 1ull)] = (int32_t)tile;
+// Persistent: the CTA takes the next `group` consecutive positions of the
+// permuted tile sequence per round (one per warp), then finishes their heavy
+// scalar ranges together, in position order.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async(DevLP L, StepParams P, PermKeys K, int64_t n_tiles,
+                                                               int group, int64_t heavy_limit,
+                                                               unsigned long long* next) {
+    __shared__ WarpSmem wsm[kWarpsPerBlock];
+    __shared__ CtaSmem csm;
+    __shared__ int64_t heavy_tile[kWarpsPerBlock];
+    __shared__ int64_t base_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (;;) {
+        // dynamic scheduling: positions are handed out in sequence order
+        if (threadIdx.x == 0) base_s = (int64_t)atomicAdd(next, (unsigned long long)group);
+        __syncthreads();
+        const int64_t base = base_s;
+        if (base >= n_tiles) break;
+        const int64_t t_idx = base + w;
+        bool heavy = false;
+        int64_t tile = -1;
+        if (w < group && t_idx < n_tiles) {
+            tile = (int64_t)tile_perm((uint64_t)t_idx, K);
+            heavy = async_tile_warp(L, P, tile, lane, wsm[w], heavy_limit);
+        }
+        if (lane == 0) heavy_tile[w] = heavy ? tile : -1;
+        __syncthreads();
+        for (int h = 0; h < group; h++) {
+            const int64_t ht = heavy_tile[h];
+            if (ht >= 0) async_tile_cta(L, P, ht, csm);
+        }
+        __syncthreads();
     }
 }
 
@@ -445,18 +514,25 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
     return cudaGetLastError() == cudaSuccess ? THETIS_OK : THETIS_ERR_CUDA;
 }
 
-static int ensure_heavy(thetis_lp* lp) {
-    if (lp->heavy_valid) return THETIS_OK;
-    const int64_t n_tiles = (lp->d.U + 31) / 32;
-    unsigned long long* cnt = (unsigned long long*)(lp->flags + 48);
-    CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, lp->stream));
-    if (n_tiles > 0) k_find_heavy<<<grid_for(n_tiles, 256), 256, 0, lp->stream>>>(lp->d, n_tiles, lp->heavy, cnt);
-    unsigned long long h = 0;
-    CUDA_TRY(lp, cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, lp->stream));
-    CUDA_TRY(lp, cudaStreamSynchronize(lp->stream));
-    lp->n_heavy = (int64_t)h;
-    lp->heavy_valid = true;
-    return THETIS_OK;
+// Bounded staleness (the async scheme needs the number of concurrent
+// updaters small relative to n): at most ~n_tiles / kAsyncDepth warps are in
+// flight (< 0.8% of the tiles), and never more than the device holds at once
+// (persistent grid); large LPs are bounded by the device, not by the depth.
+constexpr int64_t kAsyncDepth = 128;
+static int64_t async_blocks(thetis_lp* lp, int64_t n_tiles) {
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async, kWarpsPerBlock * 32, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    (void)lp;
+    int64_t depth_cap = (n_tiles + kWarpsPerBlock * kAsyncDepth - 1) / (kWarpsPerBlock * kAsyncDepth);
+    int64_t dev_cap = (int64_t)per_sm * sms;
+    int64_t b = depth_cap < dev_cap ? depth_cap : dev_cap;
+    return b < 1 ? 1 : b;
 }
 
 int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
@@ -470,7 +546,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     const double Lmax = (double)beta * lp->maxnorm2 + 1.0 / (double)beta; // Eq. 7
     P.invLmax = (float)(1.0 / Lmax);
     if (mode == THETIS_MODE_DETERMINISTIC) THETIS_TRY(ensure_colouring(lp, seed));
-    else THETIS_TRY(ensure_heavy(lp));
     const bool timed = st != nullptr;
     if (timed) {
         if (lp->ev_epoch.empty()) {
@@ -490,18 +565,13 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, s>>>(L, P);
         } else {
             PermKeys K = make_perm_keys(n_tiles, seed, e);
-            if (lp->n_heavy > 0) {
-                CUDA_TRY(lp, cudaEventRecord(lp->ev_fork, s));
-                CUDA_TRY(lp, cudaStreamWaitEvent(lp->side, lp->ev_fork, 0));
-                k_async_heavy<<<(unsigned)lp->n_heavy, kHeavyThreads, 0, lp->side>>>(L, P, lp->heavy, lp->n_heavy);
-            }
             if (n_tiles > 0) {
-                int64_t blocks = (n_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-                k_async_tiles<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, K, n_tiles);
-            }
-            if (lp->n_heavy > 0) {
-                CUDA_TRY(lp, cudaEventRecord(lp->ev_join, lp->side));
-                CUDA_TRY(lp, cudaStreamWaitEvent(s, lp->ev_join, 0));
+                const bool serial = mode == THETIS_MODE_ASYNC_SERIAL;
+                int64_t blocks = serial ? 1 : async_blocks(lp, n_tiles);
+                unsigned long long* next = (unsigned long long*)(lp->flags + 56);
+                CUDA_TRY(lp, cudaMemsetAsync(next, 0, 8, s));
+                k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, K, n_tiles,
+                                                                         serial ? 1 : kWarpsPerBlock, kHeavy, next);
             }
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));

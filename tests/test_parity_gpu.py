@@ -320,53 +320,85 @@ def test_mwc_rounding_cross_application(th):
 
 
 # ------------------------------------------------------------------ async
-@pytest.mark.parametrize("problem", [VC, MIS])
-def test_async_matches_reference_trajectory(th, problem):
-    cfg = inputs.CONFIGS["vc_er_1k"]
-    gi = inputs.make_graph(cfg)
-    g, r32, r64 = both(th, problem, gi.n, gi.src, gi.dst, vw=gi.vertex_w)
-    g.solve(10.0, 20, mode=1, seed=71)
-    r64.solve(10.0, 20, mode=1, seed=71)
-    o, ro = g.objective(10.0), r64.objective(10.0)
-    assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-3)
-    assert o["lp_obj"] == pytest.approx(ro["lp_obj"], rel=1e-3)
-    rule = 1 if problem == VC else 3
-    _, res = g.round(rule)
-    _, rres = r64.round(rule)
-    assert res["feasible"] == 1 and res["cost"] == pytest.approx(rres["cost"], rel=1e-2)
-
-
-def test_async_mwc_matches_reference_trajectory(th):
-    src, dst = grid(40)
-    ew = np.random.default_rng(5).exponential(1.0, len(src)).astype(np.float32)
-    terms = inputs.terminals(1600, 25, 6)
-    g, r32, r64 = both(th, MWC, 1600, src, dst, ew=ew, k=5, terms=terms, t=5)
-    g.solve(10.0, 30, mode=1, seed=74)
-    r64.solve(10.0, 30, mode=1, seed=74)
-    o, ro = g.objective(10.0), r64.objective(10.0)
-    assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-3)
-    assert o["lp_obj"] == pytest.approx(ro["lp_obj"], rel=1e-3)
-    _, res = g.round(4, seed=94, reps=10)
-    _, rres = r64.round(4, seed=94, reps=10)
-    assert res["cost"] == pytest.approx(rres["cost"], rel=1e-2)
-
-
-def test_async_heavy_tiles(th):
-    # hubs whose tiles exceed the warp path's nnz budget run on the CTA kernel
+def hub_graph():
     rng = np.random.default_rng(2)
     n = 20000
-    hubs = rng.integers(0, 64, 60000).astype(np.int32)
-    other = rng.integers(0, n, 60000).astype(np.int32)
-    src = np.concatenate([hubs, rng.integers(0, n, 40000).astype(np.int32)])
-    dst = np.concatenate([other, rng.integers(0, n, 40000).astype(np.int32)])
-    vw = rng.uniform(1, 10, n).astype(np.float32)
-    g, r32, r64 = both(th, VC, n, src, dst, vw=vw)
-    for rule in (0, 1):
-        g.solve(10.0, 15, mode=1, seed=5, step_rule=rule)
-        r64.solve(10.0, 15, mode=1, seed=5, step_rule=rule)
-        o, ro = g.objective(10.0), r64.objective(10.0)
-        assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-3)
-        assert o["drift_inf"] < 1e-3
+    src = np.concatenate([rng.integers(0, 64, 60000), rng.integers(0, n, 40000)]).astype(np.int32)
+    dst = np.concatenate([rng.integers(0, n, 60000), rng.integers(0, n, 40000)]).astype(np.int32)
+    return n, src, dst, rng.uniform(1, 10, n).astype(np.float32)
+
+
+def async_cases():
+    cfg = inputs.CONFIGS["vc_er_1k"]
+    gi = inputs.make_graph(cfg)
+    src, dst = grid(40)
+    ew = np.random.default_rng(5).exponential(1.0, len(src)).astype(np.float32)
+    n, hs, hd, hw = hub_graph()
+    return {
+        "vc_cfg1": dict(problem=VC, n=gi.n, src=gi.src, dst=gi.dst, vw=gi.vertex_w, epochs=20),
+        "mis_cfg1": dict(problem=MIS, n=gi.n, src=gi.src, dst=gi.dst, vw=gi.vertex_w, epochs=20),
+        "mwc_grid40": dict(problem=MWC, n=1600, src=src, dst=dst, ew=ew, k=5, terms=inputs.terminals(1600, 25, 6),
+                           t=5, epochs=30),
+        "vc_hubs": dict(problem=VC, n=n, src=hs, dst=hd, vw=hw, epochs=15),
+    }
+
+
+def build_case(th, c, bits=None):
+    kw = dict(vertex_w=c.get("vw"), edge_w=c.get("ew"), k=c.get("k", 0), terminals=c.get("terms"),
+              t_per_label=c.get("t", 0))
+    if bits is None:
+        return th.LP.from_graph(c["problem"], c["n"], c["src"], c["dst"], **kw)
+    return RefLP.graph(c["problem"], c["n"], c["src"], c["dst"], bits=bits, **kw)
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+@pytest.mark.parametrize("name", ["vc_cfg1", "mis_cfg1", "mwc_grid40", "vc_hubs"])
+def test_async_kernel_serial_equals_tile_sync_replay(th, name, rule):
+    # the async kernel with one tile in flight is the oracle's tile-synchronous
+    # replay of the same permutation (exact arithmetic check of the async path,
+    # heavy-tile CTA path and block lanes included)
+    c = async_cases()[name]
+    g = build_case(th, c)
+    r = build_case(th, c, bits=64)
+    g.solve(10.0, c["epochs"], mode=th.THETIS_MODE_ASYNC_SERIAL, seed=71, step_rule=rule)
+    r.solve(10.0, c["epochs"], mode=oracle.MODE_TILE_SYNC, seed=71, step_rule=rule)
+    assert close(g.get_x().cpu().numpy(), r.x()) and close(g.get_r().cpu().numpy(), r.r())
+
+
+@pytest.mark.parametrize("name", ["vc_cfg1", "mis_cfg1", "mwc_grid40"])
+def test_async_matches_reference_trajectory(th, name):
+    # BASELINE north star: f_beta and c^T x within 1e-3 of the oracle's async
+    # reference trajectory (R-6: the tile-synchronous replay), rounded cost within 1%
+    c = async_cases()[name]
+    g = build_case(th, c)
+    r = build_case(th, c, bits=64)
+    g.solve(10.0, c["epochs"], mode=1, seed=71)
+    r.solve(10.0, c["epochs"], mode=oracle.MODE_TILE_SYNC, seed=71)
+    o, ro = g.objective(10.0), r.objective(10.0)
+    assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-3)
+    assert o["lp_obj"] == pytest.approx(ro["lp_obj"], rel=1e-3)
+    rule, kw = {VC: (1, {}), MIS: (3, {}), MWC: (4, dict(seed=94, reps=10))}[c["problem"]]
+    _, res = g.round(rule, **kw)
+    _, rres = r.round(rule, **kw)
+    assert res["feasible"] == 1 and res["cost"] == pytest.approx(rres["cost"], rel=1e-2)
+    assert o["drift_inf"] < 1e-4
+
+
+def test_async_hub_stress_bounded_deviation(th):
+    # stress case outside the BASELINE configs: 64 hubs carry a third of all rows and
+    # ~3% of the tiles are in flight, so Hogwild staleness moves f_beta by < 1% from the
+    # reference trajectory (it converges to the same x(beta); R-6)
+    c = async_cases()["vc_hubs"]
+    g = build_case(th, c)
+    r = build_case(th, c, bits=64)
+    g.solve(10.0, c["epochs"], mode=1, seed=71)
+    r.solve(10.0, c["epochs"], mode=oracle.MODE_TILE_SYNC, seed=71)
+    o, ro = g.objective(10.0), r.objective(10.0)
+    assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-2)
+    _, res = g.round(1)
+    _, rres = r.round(1)
+    assert res["feasible"] == 1 and res["cost"] == pytest.approx(rres["cost"], rel=2e-2)
+    assert o["drift_inf"] < 1e-3
 
 
 # ------------------------------------------------------------------ edge cases / errors
