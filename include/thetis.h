@@ -125,7 +125,8 @@ THETIS_API int thetis_build_graph_lp_workspace(int problem, int64_t n, int64_t n
  *  src, dst   int32[n_edges] endpoints in [0, n); orientation free; self-loops
  *             dropped; duplicate pairs kept once (the first occurrence's
  *             edge weight is used).  Rows follow the unique canonical pairs
- *             (u < v) in (u, v) order.
+ *             (u < v) in (v, u) order (a vertex's edges to smaller ids are one
+ *             contiguous run of rows).
  *  vertex_w   float[n]: VC costs c_v (min) / MIS weights w_v (max).
  *  edge_w     float[n_edges]: MWC edge costs c_uv (objective 1/2 sum c_uv sum_l x_uv^l).
  *  k          MWC labels (2..32); terminals int32[k * t_per_label], label-major

@@ -19,6 +19,7 @@
 #endif
 
 #define GOLDEN 0x9E3779B97F4A7C15ULL
+#define HUB_NNZ 2048 /* R-6: tiles whose scalar columns hold more nonzeros are hub tiles */
 
 enum { PROB_GENERIC = 0, PROB_VC = 1, PROB_MIS = 2, PROB_MWC = 3 };
 enum { SENSE_EQ = 0, SENSE_GE = 1, SENSE_LE = 2 };
@@ -320,15 +321,15 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     for (int64_t e = 0; e < n_edges; e++)
         if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) return REF_INVALID_ARG;
 
-    /* canonicalise (u < v), drop self-loops, sort by (u, v), keep the first
-     * occurrence of each pair: the rows in "CSR-upper" order */
+    /* canonicalise (u < v), drop self-loops, sort by (v, u), keep the first
+     * occurrence of each pair: the row order (R-17) */
     keyed_edge* ke = (keyed_edge*)xcalloc(n_edges, sizeof(keyed_edge));
     int64_t cnt = 0;
     for (int64_t e = 0; e < n_edges; e++) {
         uint64_t u = (uint64_t)src[e], v = (uint64_t)dst[e];
         if (u == v) continue;
         if (u > v) { uint64_t t = u; u = v; v = t; }
-        ke[cnt].key = (u << 32) | v;
+        ke[cnt].key = (v << 32) | u;
         ke[cnt].idx = e;
         cnt++;
     }
@@ -344,8 +345,8 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     lp->eu = (int32_t*)xcalloc(me, sizeof(int32_t));
     lp->ev = (int32_t*)xcalloc(me, sizeof(int32_t));
     for (int64_t e = 0; e < me; e++) {
-        lp->eu[e] = (int32_t)(ke[e].key >> 32);
-        lp->ev[e] = (int32_t)(ke[e].key & 0xFFFFFFFFu);
+        lp->eu[e] = (int32_t)(ke[e].key & 0xFFFFFFFFu);
+        lp->ev[e] = (int32_t)(ke[e].key >> 32);
     }
     if (problem == PROB_MWC) {
         lp->ew = (float*)xcalloc(me, sizeof(float));
@@ -769,7 +770,28 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                 if (colour[u] == cl) order[n_order++] = u;
     }
     int64_t n_tiles = (lp->U + 31) / 32;
+    const int64_t n_struct_units = lp->n_blocks + lp->n_scalar;
+    const int64_t n_struct_tiles = (n_struct_units + 31) / 32;
     int64_t* perm = (mode == MODE_ASYNC || mode == 3) ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
+    /* hub tiles of the async reference (R-6): VC / MIS tiles whose scalar
+     * columns hold more than HUB_NNZ nonzeros */
+    uint8_t* hub_tile = NULL;
+    int64_t* hub_cols = NULL;
+    REAL* hub_new = NULL;
+    int64_t n_hub_cols = 0;
+    if (mode == 3 && (lp->problem == PROB_VC || lp->problem == PROB_MIS)) {
+        hub_tile = (uint8_t*)xcalloc(n_struct_tiles, 1);
+        hub_cols = (int64_t*)xcalloc(n_struct_tiles * 32, sizeof(int64_t));
+        for (int64_t t = 0; t < n_struct_tiles; t++) {
+            int64_t nz = 0;
+            for (int64_t u = t * 32; u < t * 32 + 32 && u < lp->n_scalar; u++) nz += col_nnz(lp, u);
+            if (nz > HUB_NNZ) {
+                hub_tile[t] = 1;
+                for (int64_t u = t * 32; u < t * 32 + 32 && u < lp->n_scalar; u++) hub_cols[n_hub_cols++] = u;
+            }
+        }
+        hub_new = (REAL*)xcalloc(n_hub_cols, sizeof(REAL));
+    }
     for (int e = 0; e < epochs; e++) {
         if (mode == MODE_DET) {
             for (int64_t p = 0; p < n_order; p++) {
@@ -790,10 +812,33 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                 }
         } else if (mode == 3) {
             REAL nv[32 * 64];
-            thetis_ref_tile_perm(n_tiles, seed, e, perm);
-            for (int64_t t = 0; t < n_tiles; t++) {
-                int64_t u1 = perm[t] * 32 + 32 < lp->U ? perm[t] * 32 + 32 : lp->U;
-                nnz += step_tile_sync(lp, &s, perm[t] * 32, u1, &updates, nv);
+            /* (1) hub step (VC / MIS): the scalar columns of every hub tile take one
+             * synchronous step from the epoch's starting state */
+            if (hub_cols) {
+                for (int64_t q = 0; q < n_hub_cols; q++) {
+                    REAL v[1];
+                    unit_new_values(lp, &s, hub_cols[q], v);
+                    hub_new[q] = v[0];
+                }
+                for (int64_t q = 0; q < n_hub_cols; q++) {
+                    int64_t u = hub_cols[q];
+                    if (unit_fixed(lp, u)) continue;
+                    nnz += apply_unit(lp, u, &hub_new[q]);
+                    updates += 1;
+                }
+            }
+            /* (2) slack sweep: slacks share no row, so any order gives the same result */
+            for (int64_t u = n_struct_units; u < lp->U; u++) {
+                nnz += step_unit(lp, &s, u);
+                updates += 1;
+            }
+            /* (3) tiles of structural units in permutation order, each one synchronous
+             * step of its units (hub tiles have no units left) */
+            thetis_ref_tile_perm(n_struct_tiles, seed, e, perm);
+            for (int64_t t = 0; t < n_struct_tiles; t++) {
+                if (hub_tile && hub_tile[perm[t]]) continue;
+                int64_t u0 = perm[t] * 32, u1 = u0 + 32 < n_struct_units ? u0 + 32 : n_struct_units;
+                nnz += step_tile_sync(lp, &s, u0, u1, &updates, nv);
             }
         } else {
             for (int64_t u = 0; u < lp->U; u++) {
@@ -805,7 +850,7 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
             }
         }
     }
-    free(colour); free(order); free(perm);
+    free(colour); free(order); free(perm); free(hub_tile); free(hub_cols); free(hub_new);
     if (st) {
         st->epochs = epochs;
         st->coordinate_updates = updates;

@@ -96,9 +96,13 @@ double thetis_ref_grad(const ref_lp* lp, float beta, int64_t j);
  * mode 1 = unit-sequential replay of the tile permutation (Alg. 1 one
  *          coordinate at a time, in the async order);
  * mode 2 = plain cyclic sweep;
- * mode 3 = the async reference trajectory (R-6): tiles in permutation order,
- *          each tile one synchronous step of its 32 units (every unit steps
- *          from the state at the tile's start, then all are applied). */
+ * mode 3 = the async reference trajectory (R-6), per epoch: (1) VC / MIS:
+ *          the scalar columns of the hub tiles (tiles of 32 structural units
+ *          whose columns hold > 2048 nonzeros) take one synchronous step;
+ *          (2) every slack takes its step (slacks share no row); (3) the tiles
+ *          of 32 structural units in permutation order (pi_e over the
+ *          structural tiles), each one synchronous step of its units (every
+ *          unit steps from the state at the tile's start), hub tiles skipped. */
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                      int step_rule, ref_stats* st);
 int thetis_ref_objective(const ref_lp* lp, float beta, ref_objective* out);

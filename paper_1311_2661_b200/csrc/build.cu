@@ -2,6 +2,8 @@
 // LP in HBM (CSC with sign-bit coefficients, unique edge rows, costs, bounds), the
 // initial point z0 with r0 = A z0 - b, and max ||a_j||^2 for L_max (Eq. 7).
 //
+//   rows: one per unique undirected non-loop edge (u < v), ordered by (v, u), so
+//   that a vertex's edges to smaller ids form one contiguous run of rows
 //   VC  (Eq. 2):   row e = (u < v): x_u + x_v - s_e = 1
 //   MIS (App. B.2):           row e:           x_u + x_v + s_e = 1, max w^T x
 //   MWC (App. B.3): x_v^l at v*k+l, x_e^l at n*k+e*k+l;
@@ -36,7 +38,7 @@ __global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ sr
             keys[i] = sent; // self-loop: sorts last, dropped
         } else {
             uint64_t a = (uint64_t)(u < v ? u : v), b = (uint64_t)(u < v ? v : u);
-            keys[i] = a * (uint64_t)n + b;
+            keys[i] = b * (uint64_t)n + a; // rows in (max, min) order
         }
         if (idx) idx[i] = (int32_t)i;
     }
@@ -45,23 +47,24 @@ __global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ sr
 __global__ void k_decode_edges(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
-        edges[e] = make_int2((int32_t)(k / (uint64_t)n), (int32_t)(k % (uint64_t)n));
+        edges[e] = make_int2((int32_t)(k % (uint64_t)n), (int32_t)(k / (uint64_t)n)); // (min, max)
     }
 }
-// (v, e) pairs for the stable by-v sort (lower incidences)
+// (min endpoint, e) pairs for the stable by-min sort (the scattered incidences)
 __global__ void k_vkeys(int64_t m, const int2* __restrict__ edges, int32_t* __restrict__ vkey, int32_t* __restrict__ eval) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        vkey[e] = edges[e].y;
+        vkey[e] = edges[e].x;
         eval[e] = (int32_t)e;
     }
 }
 
 // run boundaries of a sorted key sequence: start[key] = first pos, end[key] = last pos + 1
+// rows come in runs of equal max endpoint
 __global__ void k_runs_u(int64_t m, const int2* __restrict__ edges, int32_t* start, int32_t* end) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        int u = edges[e].x;
-        if (e == 0 || edges[e - 1].x != u) start[u] = (int32_t)e;
-        if (e == m - 1 || edges[e + 1].x != u) end[u] = (int32_t)(e + 1);
+        int u = edges[e].y;
+        if (e == 0 || edges[e - 1].y != u) start[u] = (int32_t)e;
+        if (e == m - 1 || edges[e + 1].y != u) end[u] = (int32_t)(e + 1);
     }
 }
 __global__ void k_runs_key(int64_t m, const int32_t* __restrict__ key, int32_t* start, int32_t* end) {
@@ -76,21 +79,22 @@ __global__ void k_degrees(int64_t n, const int32_t* us, const int32_t* ue, const
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x)
         deg[v] = v < n ? (int64_t)(ue[v] - us[v]) + (int64_t)(le[v] - ls[v]) : 0;
 }
-// incidence lists in ascending edge order: lower incidences (v = ev[e]) come
-// first (their rows precede the upper run of v), then the upper run.
+// incidence lists in ascending row order: the run of rows where the vertex is the
+// max endpoint (contiguous, smaller row ids) comes first, then the rows where it is
+// the min endpoint (scattered; stable by-min sort keeps them ascending).
 __global__ void k_fill_lower(int64_t m, const int32_t* __restrict__ vkey, const int32_t* __restrict__ eval,
+                             const int32_t* __restrict__ us, const int32_t* __restrict__ ue,
                              const int32_t* __restrict__ ls, const int64_t* __restrict__ iptr, int32_t* inc) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
         int v = vkey[p];
-        inc[iptr[v] + (p - ls[v])] = eval[p];
+        inc[iptr[v] + (ue[v] - us[v]) + (p - ls[v])] = eval[p];
     }
 }
 __global__ void k_fill_upper(int64_t m, const int2* __restrict__ edges, const int32_t* __restrict__ us,
-                             const int32_t* __restrict__ ls, const int32_t* __restrict__ le,
                              const int64_t* __restrict__ iptr, int32_t* inc) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        int u = edges[e].x;
-        inc[iptr[u] + (le[u] - ls[u]) + (e - us[u])] = (int32_t)e;
+        int u = edges[e].y;
+        inc[iptr[u] + (e - us[u])] = (int32_t)e;
     }
 }
 
@@ -399,7 +403,7 @@ static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* 
     uint8_t* unit_fixed = mwc ? C.take<uint8_t>(S) : nullptr;
     int32_t* colour = C.take<int32_t>(S);
     int32_t* members = C.take<int32_t>(S);
-    int32_t* heavy = C.take<int32_t>((U + kTile - 1) / kTile);
+    int32_t* heavy = C.take<int32_t>(2 * ((U + kTile - 1) / kTile) + 2);
     double* red = C.take<double>(kRedBlocks * 16 + 256);
     int32_t* flags = C.take<int32_t>(64);
     // temporaries of the build, reused afterwards by colouring and rounding
@@ -476,7 +480,7 @@ static size_t generic_layout(int64_t m, int64_t n, int64_t nnz, bool has_val, th
     float* ua = C.take<float>(n);
     int32_t* colour = C.take<int32_t>(S);
     int32_t* members = C.take<int32_t>(S);
-    int32_t* heavy = C.take<int32_t>((U + kTile - 1) / kTile);
+    int32_t* heavy = C.take<int32_t>(2 * ((U + kTile - 1) / kTile) + 2);
     double* red = C.take<double>(kRedBlocks * 16 + 256);
     int32_t* flags = C.take<int32_t>(64);
     size_t temp_start = (C.off + 255) & ~(size_t)255;
@@ -634,8 +638,8 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
         CUDA_TRY(lp, cub::DeviceScan::ExclusiveSum(t.cub, cb, t.deg, iptr, n + 1, s));
     }
     if (m > 0) {
-        k_fill_lower<<<grid_for(m, T), T, 0, s>>>(m, vsorted, esorted, t.ls, iptr, inc);
-        k_fill_upper<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, t.ls, t.le, iptr, inc);
+        k_fill_lower<<<grid_for(m, T), T, 0, s>>>(m, vsorted, esorted, t.us, t.ue, t.ls, iptr, inc);
+        k_fill_upper<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, iptr, inc);
     }
     THETIS_TRY(check_cuda(lp, "build: incidence"));
 

@@ -15,21 +15,25 @@
 // fp32 build of the oracle.
 //
 // Async mode (R-6): tiles of 32 consecutive units in a per-epoch keyed
-// permutation; one persistent kernel, a warp per tile, tile-synchronous inside
-// the tile (all gathers, then all scatters), Hogwild across tiles: r is read
-// with L2 loads (ld.global.cg; stale values allowed) and written with
-// red.global.add.f32, so no update is lost.  Scalar-column tiles are processed
-// cooperatively: the tile's nonzeros are one contiguous CSC range, read
-// coalesced 32 at a time; a tile with more than kHeavy nonzeros is finished by
-// its whole CTA at its place in the sequence.  The grid bounds the number of
-// tiles in flight to ~n_tiles / kAsyncDepth (bounded staleness).
+// permutation; one persistent kernel whose warps are independent workers.  A
+// tile is tile-synchronous (all gathers, then all scatters); tiles run
+// concurrently, Hogwild-style: r is read with L2 loads (ld.global.cg; stale
+// values allowed) and written with red.global.add.f32, so no update is lost.
+// A tile's scalar columns are one contiguous CSC range, read coalesced 32 at a
+// time (register accumulation inside a column, shared atomics across column
+// boundaries).  A tile with more than kHeavy nonzeros (power-law hubs) is split
+// into kChunk pieces that any warp may claim: warps help finish pending heavy
+// tiles (FIFO in draw order) before drawing new positions.  The grid bounds the
+// number of workers to ~n_tiles / kAsyncDepth (bounded staleness).
+#include <cub/cub.cuh>
+
 #include "thetis_internal.cuh"
 
 namespace thetis {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int64_t kHeavy = 2048;    // async: scalar nnz per tile above which a CTA takes it
+constexpr int64_t kHeavy = 2048;    // async: scalar nnz per tile above which the tile is split
 constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the warp path
 
 struct StepParams {
@@ -159,27 +163,27 @@ __device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParam
     }
 }
 
-// slack q of row i: a = sigma_i e_i, cost 0, bounds [0, inf)
-template <bool kAsync>
+// slack of row i (column j): a = sigma_i e_i, cost 0, bounds [0, inf); the new
+// value from the row's residual rv
+__device__ __forceinline__ float slack_new(const DevLP& L, const StepParams& P, int64_t i, int64_t j, float sig,
+                                           float rv, float z) {
+    float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
+    float ua = 0.0f;
+    if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[i] : L.ubar[i]);
+    float g = grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
+    float t = __fsub_rn(z, __fmul_rn(g, unit_invL(P, 1.0)));
+    return t < 0.0f ? 0.0f : t;
+}
+// one slack step with a plain read-modify-write of r (rows of distinct slacks differ)
 __device__ __forceinline__ void update_slack(const DevLP& L, const StepParams& P, int64_t q) {
     const int64_t i = slack_row_of(L, q);
     const int64_t j = L.n_s + q;
     const float sig = row_sigma(L, i);
-    float rv = kAsync ? ld_cg(L.r + i) : L.r[i];
-    float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
-    float ua = 0.0f;
-    if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[i] : L.ubar[i]);
-    float z = L.z[j];
-    float g = grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
-    float invL = unit_invL(P, 1.0);
-    float t = __fsub_rn(z, __fmul_rn(g, invL));
-    float zn = t < 0.0f ? 0.0f : t;
-    float d = __fsub_rn(zn, z);
-    if (d != 0.0f) {
-        float ad = sig < 0.0f ? -d : d;
-        if (kAsync) red_add(L.r + i, ad);
-        else L.r[i] = __fadd_rn(L.r[i], ad);
-    }
+    const float rv = L.r[i];
+    const float z = L.z[j];
+    const float zn = slack_new(L, P, i, j, sig, rv, z);
+    const float d = __fsub_rn(zn, z);
+    if (d != 0.0f) L.r[i] = __fadd_rn(rv, sig < 0.0f ? -d : d);
     L.z[j] = zn;
 }
 
@@ -244,11 +248,13 @@ __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const 
 
 __global__ void __launch_bounds__(256) k_det_slacks(DevLP L, StepParams P) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L.n_ineq; q += (int64_t)gridDim.x * blockDim.x)
-        update_slack<false>(L, P, q);
+        update_slack(L, P, q);
 }
 
 // ------------------------------------------------------------ async
-// scalar sub-range [a, b) of the tile's lanes
+constexpr int kBatch = 16;         // permuted positions drawn per atomic by a warp (large grids)
+
+// scalar sub-range [a, b) of the tile's lanes (tiles cover the structural units)
 __device__ __forceinline__ void scalar_lanes(const DevLP& L, int64_t u0, int& a, int& b) {
     const int64_t s0 = L.n_blocks, s1 = L.n_blocks + L.n_scalar;
     int64_t lo = u0 > s0 ? u0 : s0, hi = u0 + 32 < s1 ? u0 + 32 : s1;
@@ -278,107 +284,259 @@ __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P
     project_simplex(y, k, x);
 }
 
+// per-warp shared state
 struct WarpSmem {
-    float acc[32];
-    float d[32];
-    int32_t head[32];
+    int64_t cp[33];   // column starts of the tile's scalar range (cp[ncols] = end)
+    float acc[32];    // per-column partial dots
+    float d[32];      // per-column steps
 };
 
-// column (lane index) of the nonzero at position base + lane: the segment heads
-// falling in the chunk, max-scanned, carried over from the previous chunk
-__device__ __forceinline__ int chunk_col(int lane, int ncols, int64_t cp, int64_t base, int64_t end, int32_t* head,
-                                         int& carry) {
-    head[lane] = -1;
+struct TileCols {
+    int64_t j0, u0;
+    int a, ncols;
+};
+
+__device__ __forceinline__ TileCols load_cols(const DevLP& L, int64_t tile, WarpSmem& sm, int lane) {
+    TileCols tc;
+    tc.u0 = tile * 32;
+    int b;
+    scalar_lanes(L, tc.u0, tc.a, b);
+    tc.ncols = b - tc.a;
+    tc.j0 = L.n_blocks * L.k + (tc.u0 + tc.a - L.n_blocks);
+    if (tc.ncols > 0)
+        for (int i = lane; i <= tc.ncols; i += 32) sm.cp[i] = L.colptr[tc.j0 + i];
     __syncwarp();
-    if (lane < ncols && cp >= base && cp < base + 32 && cp < end) atomicMax(&head[(int)(cp - base)], lane);
-    __syncwarp();
-    int col = head[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int x = __shfl_up_sync(0xffffffffu, col, o);
-        if (lane >= o) col = x > col ? x : col;
-    }
-    col = col > carry ? col : carry;
-    carry = __shfl_sync(0xffffffffu, col, 31);
-    __syncwarp();
-    return col;
+    return tc;
 }
 
-// One tile, one warp, tile-synchronous: every unit of the tile gathers from the
-// residual as it is when the tile starts (stale w.r.t. other tiles in flight),
-// then all units scatter.  Scalar columns are processed cooperatively over the
-// tile's contiguous CSC range.  Returns true (warp-uniform) when the scalar range
-// has more than heavy_limit nonzeros: the whole CTA then finishes it.
-__device__ __forceinline__ bool async_tile_warp(const DevLP& L, const StepParams& P, int64_t tile, int lane,
-                                                WarpSmem& sm, int64_t heavy_limit) {
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// largest column index c with cp[c] <= t (uniform over the warp)
+__device__ __forceinline__ int col_of(const WarpSmem& sm, int ncols, int64_t t) {
+    int lo = 0, hi = ncols - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__device__ __forceinline__ float nz_value(const DevLP& L, int64_t t) {
+    int64_t row;
+    float av;
+    entry(L, t, row, av);
+    float rv = ld_cg(L.r + row);
+    return L.val ? av * rv : (av < 0.0f ? -rv : rv);
+}
+__device__ __forceinline__ void nz_scatter(const DevLP& L, int64_t t, float d) {
+    int64_t row;
+    float av;
+    entry(L, t, row, av);
+    red_add(L.r + row, L.val ? av * d : (av < 0.0f ? -d : d));
+}
+
+// partial dots of the tile's columns over the nonzero range [c0, c1), added into
+// sm.acc.  Sub-chunks of 32 lying inside one column accumulate in registers;
+// mixed sub-chunks locate each lane's column and add with shared atomics.
+__device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
+                                             int lane) {
+    int c = col_of(sm, ncols, c0);
+    int64_t nb = sm.cp[c + 1];
+    float acc = 0.0f;
+    for (int64_t base = c0; base < c1; base += 32) {
+        if (nb <= base) {
+            acc = warp_sum(acc);
+            if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
+            acc = 0.0f;
+            do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+        }
+        const int64_t t = base + lane;
+        if (base + 32 <= nb || c1 <= nb) {
+            if (t < c1) acc += nz_value(L, t);
+        } else if (t < c1) {
+            int col = c;
+            while (sm.cp[col + 1] <= t) col++;
+            atomicAdd(&sm.acc[col], nz_value(L, t));
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
+    __syncwarp();
+}
+// r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]
+__device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
+                                              int lane) {
+    int c = col_of(sm, ncols, c0);
+    int64_t nb = sm.cp[c + 1];
+    float dc = sm.d[c];
+    for (int64_t base = c0; base < c1; base += 32) {
+        if (nb <= base) {
+            do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+            dc = sm.d[c];
+        }
+        const int64_t t = base + lane;
+        if (base + 32 <= nb || c1 <= nb) {
+            if (t < c1 && dc != 0.0f) nz_scatter(L, t, dc);
+        } else if (t < c1) {
+            int col = c;
+            while (sm.cp[col + 1] <= t) col++;
+            const float d = sm.d[col];
+            if (d != 0.0f) nz_scatter(L, t, d);
+        }
+    }
+}
+
+// the coordinate step of lane's column from D = sm.acc[lane]; returns the change
+__device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P, const TileCols& tc, float D,
+                                             int lane) {
+    if (lane >= tc.ncols || (L.unit_fixed && L.unit_fixed[tc.u0 + tc.a + lane])) return 0.0f;
+    const int64_t j = tc.j0 + lane;
+    float z = L.z[j];
+    float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
+    float invL = unit_invL(P, col_norm2(L, j));
+    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
+    L.z[j] = zn;
+    return __fsub_rn(zn, z);
+}
+
+// Hub step (R-6): tiles whose scalar columns hold more than kHeavy nonzeros take
+// one synchronous block step at the start of the epoch.  For VC / MIS (every row
+// = one edge (u, v) with coefficients +1, and a synchronous step with 1/L_max is
+// a descent step) it runs as two coalesced streams over the rows: the gather
+// adds r_e into the (L2-resident) accumulators of the hub endpoints, the update
+// takes the hub steps, the scatter adds the hub steps of both endpoints to r_e
+// with a plain read-modify-write (the hub phase runs alone).
+struct HubCtx {
+    int64_t n_heavy;
+    const int32_t* heavy_tiles;  // sorted tile ids
+    const uint8_t* hub_tile;     // per tile: 1 if hub tile
+    float* buf;                  // per vertex: partial dot, then step (hub vertices only)
+};
+__device__ __forceinline__ bool is_hub(const HubCtx& H, int32_t v) { return H.hub_tile[v >> 5] != 0; }
+
+// the accumulators of vertices below kPriv (where the natural-id power-law
+// generators put their biggest hubs) are privatised per CTA in shared memory:
+// the top hubs take ~1e6 additions per epoch, too many for one L2 address
+constexpr int kPriv = 8192;
+__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H) {
+    __shared__ float priv[kPriv];
+    for (int i = threadIdx.x; i < kPriv; i += blockDim.x) priv[i] = 0.0f;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e - lane < L.m; e += stride) {
+        int2 uv = make_int2(0, 0);
+        float rv = 0.0f;
+        bool hu = false, hv = false;
+        if (e < L.m) {
+            uv = L.edges[e];
+            hu = is_hub(H, uv.x);
+            hv = is_hub(H, uv.y);
+            if (hu || hv) rv = L.r[e];
+        }
+        if (hu) {
+            if (uv.x < kPriv) atomicAdd(priv + uv.x, rv);
+            else atomicAdd(H.buf + uv.x, rv);
+        }
+        // rows come in runs of equal max endpoint v (hub-ness is constant on a
+        // run): segmented suffix sums over the warp, one addition per run segment
+        float sv = hv ? rv : 0.0f;
+        const int key = hv ? uv.y : -1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float x = __shfl_down_sync(0xffffffffu, sv, o);
+            const int k2 = __shfl_down_sync(0xffffffffu, key, o);
+            if (lane + o < 32 && k2 == key) sv += x;
+        }
+        const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+        if (hv && (lane == 0 || prev != key)) {
+            if (uv.y < kPriv) atomicAdd(priv + uv.y, sv);
+            else atomicAdd(H.buf + uv.y, sv);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPriv; i += blockDim.x)
+        if (priv[i] != 0.0f) atomicAdd(H.buf + i, priv[i]);
+}
+// the hub steps: buf[j] holds D_j on entry and the step d_j on exit
+__global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= H.n_heavy * 32) return;
+    const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
+    if (j >= L.n_scalar) return;
+    float z = L.z[j];
+    float g = grad_from(c_int(L, j), ua_of(L, j), H.buf[j], z, zbar_of(L, j), P.beta);
+    float invL = unit_invL(P, col_norm2(L, j));
+    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
+    L.z[j] = zn;
+    H.buf[j] = __fsub_rn(zn, z);
+}
+// (2) fused with the end of (1): per row, add the hub steps of both endpoints to
+// r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has
+// slack column n + e); one read-modify-write of r and s per row
+__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += stride) {
+        const int2 uv = L.edges[e];
+        float delta = 0.0f;
+        if (is_hub(H, uv.x)) delta = H.buf[uv.x];
+        if (is_hub(H, uv.y)) delta = __fadd_rn(delta, H.buf[uv.y]);
+        const float r0 = L.r[e];
+        float rv = delta != 0.0f ? __fadd_rn(r0, delta) : r0;
+        const int64_t j = L.n_s + e;
+        const float sig = row_sigma(L, e);
+        const float z = L.z[j];
+        const float zn = slack_new(L, P, e, j, sig, rv, z);
+        const float d = __fsub_rn(zn, z);
+        if (d != 0.0f) rv = __fadd_rn(rv, sig < 0.0f ? -d : d);
+        if (rv != r0) L.r[e] = rv;
+        if (d != 0.0f) L.z[j] = zn;
+    }
+}
+// (2) without a hub step: the slack sweep
+__global__ void __launch_bounds__(256) k_slack_sweep(DevLP L, StepParams P) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L.n_ineq; q += (int64_t)gridDim.x * blockDim.x)
+        update_slack(L, P, q);
+}
+__global__ void k_zero_hub_buf(HubCtx H) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < H.n_heavy * 32) H.buf[(int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31)] = 0.0f;
+}
+
+struct AsyncCtx {
+    PermKeys K;
+    int64_t n_tiles, heavy_limit;  // tiles above heavy_limit were done by the hub step
+    unsigned long long* next;      // position counters (one per stream, 256 B apart)
+    int streams;
+};
+
+// (3) One tile of structural units by one warp, tile-synchronous: all units
+// gather (stale w.r.t. other tiles in flight), then all scatter.  A hub tile's
+// scalar range was stepped by the hub step of this epoch and is skipped.
+__device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx& C, int64_t tile, WarpSmem& sm,
+                             int lane) {
     const int64_t u0 = tile * 32, u = u0 + lane;
-    const bool is_block = u < L.U && u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
-    const bool is_slack = u < L.U && u >= L.n_blocks + L.n_scalar;
+    const bool is_block = u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
     float xb[kMaxK];
     if (is_block) block_values(L, P, u, xb);
-    float ds = 0.0f, sig = 0.0f;
-    int64_t srow = 0;
-    if (is_slack) {
-        const int64_t q = u - L.n_blocks - L.n_scalar, j = L.n_s + q;
-        srow = slack_row_of(L, q);
-        sig = row_sigma(L, srow);
-        float rv = ld_cg(L.r + srow);
-        float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
-        float ua = 0.0f;
-        if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[srow] : L.ubar[srow]);
-        float z = L.z[j];
-        float g = grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
-        float t = __fsub_rn(z, __fmul_rn(g, unit_invL(P, 1.0)));
-        float zn = t < 0.0f ? 0.0f : t;
-        ds = __fsub_rn(zn, z);
-        L.z[j] = zn;
-    }
-    // scalar columns
-    int a, b;
-    scalar_lanes(L, u0, a, b);
-    const int ncols = b - a;
-    bool heavy = false, coop = false;
-    int64_t j0 = 0, cp = 0, beg = 0, end = 0;
-    if (ncols > 0) {
-        j0 = L.n_blocks * L.k + (u0 + a - L.n_blocks);
-        cp = lane < ncols ? L.colptr[j0 + lane] : 0;
-        beg = __shfl_sync(0xffffffffu, cp, 0);
-        end = L.colptr[j0 + ncols];
-        heavy = end - beg > heavy_limit;
-        coop = !heavy;
-    }
+    TileCols tc = load_cols(L, tile, sm, lane);
     unsigned moved = 0;
-    if (coop) {
-        sm.acc[lane] = 0.0f;
-        __syncwarp();
-        int carry = 0;
-        for (int64_t base = beg; base < end; base += 32) {
-            const int col = chunk_col(lane, ncols, cp, base, end, sm.head, carry);
-            const int64_t t = base + lane;
-            if (t < end) {
-                int64_t row;
-                float av;
-                entry(L, t, row, av);
-                float rv = ld_cg(L.r + row);
-                atomicAdd(&sm.acc[col], L.val ? av * rv : (av < 0.0f ? -rv : rv));
-            }
+    int64_t beg = 0, end = 0;
+    if (tc.ncols > 0) {
+        beg = sm.cp[0];
+        end = sm.cp[tc.ncols];
+        if (end - beg <= C.heavy_limit) {
+            sm.acc[lane] = 0.0f;
+            __syncwarp();
+            gather_range(L, sm, tc.ncols, beg, end, lane);
+            const float d = scalar_step(L, P, tc, sm.acc[lane], lane);
+            sm.d[lane] = d;
+            moved = __ballot_sync(0xffffffffu, d != 0.0f);
         }
-        __syncwarp();
-        float d = 0.0f;
-        if (lane < ncols && !(L.unit_fixed && L.unit_fixed[u0 + a + lane])) {
-            const int64_t j = j0 + lane;
-            float z = L.z[j];
-            float g = grad_from(c_int(L, j), ua_of(L, j), sm.acc[lane], z, zbar_of(L, j), P.beta);
-            float invL = unit_invL(P, col_norm2(L, j));
-            float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-            d = __fsub_rn(zn, z);
-            L.z[j] = zn;
-        }
-        sm.d[lane] = d;
-        moved = __ballot_sync(0xffffffffu, d != 0.0f);
     }
     __syncwarp();
-    // scatter phase
     if (is_block) {
         for (int l = 0; l < L.k; l++) {
             const int64_t j = u * L.k + l;
@@ -387,116 +545,55 @@ __device__ __forceinline__ bool async_tile_warp(const DevLP& L, const StepParams
             L.z[j] = xb[l];
         }
     }
-    if (is_slack && ds != 0.0f) red_add(L.r + srow, sig < 0.0f ? -ds : ds);
-    if (moved) {
-        int carry = 0;
-        for (int64_t base = beg; base < end; base += 32) {
-            const int col = chunk_col(lane, ncols, cp, base, end, sm.head, carry);
-            const int64_t t = base + lane;
-            const float dc = sm.d[col];
-            if (t < end && dc != 0.0f) {
-                int64_t row;
-                float av;
-                entry(L, t, row, av);
-                red_add(L.r + row, L.val ? av * dc : (av < 0.0f ? -dc : dc));
-            }
-        }
-    }
-    return heavy;
+    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane);
+    __syncwarp();
 }
 
-struct CtaSmem {
-    float acc[32];
-    float d[32];
-    int64_t cp[33];
-};
-
-// the scalar range of a heavy tile, by the whole CTA (all threads call this)
-__device__ __forceinline__ void async_tile_cta(const DevLP& L, const StepParams& P, int64_t tile, CtaSmem& sm) {
-    const int64_t u0 = tile * 32;
-    int a, b;
-    scalar_lanes(L, u0, a, b);
-    const int64_t j0 = L.n_blocks * L.k + (u0 + a - L.n_blocks);
-    const int ncols = b - a;
-    if (threadIdx.x <= (unsigned)ncols) sm.cp[threadIdx.x] = L.colptr[j0 + threadIdx.x];
-    if (threadIdx.x < 32) sm.acc[threadIdx.x] = 0.0f;
-    __syncthreads();
-    const int64_t beg = sm.cp[0], end = sm.cp[ncols];
-    for (int64_t t = beg + threadIdx.x; t < end; t += blockDim.x) {
-        int lo = 0, hi = ncols - 1; // last column with start <= t
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        int64_t row;
-        float av;
-        entry(L, t, row, av);
-        float rv = ld_cg(L.r + row);
-        atomicAdd(&sm.acc[lo], L.val ? av * rv : (av < 0.0f ? -rv : rv));
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float d = 0.0f;
-        const int lane = threadIdx.x;
-        if (lane < ncols && !(L.unit_fixed && L.unit_fixed[u0 + a + lane])) {
-            const int64_t j = j0 + lane;
-            float z = L.z[j];
-            float g = grad_from(c_int(L, j), ua_of(L, j), sm.acc[lane], z, zbar_of(L, j), P.beta);
-            float invL = unit_invL(P, col_norm2(L, j));
-            float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-            d = __fsub_rn(zn, z);
-            L.z[j] = zn;
-        }
-        sm.d[lane] = d;
-    }
-    __syncthreads();
-    for (int64_t t = beg + threadIdx.x; t < end; t += blockDim.x) {
-        int lo = 0, hi = ncols - 1;
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        float dc = sm.d[lo];
-        if (dc == 0.0f) continue;
-        int64_t row;
-        float av;
-        entry(L, t, row, av);
-        red_add(L.r + row, L.val ? av * dc : (av < 0.0f ? -dc : dc));
-    }
-    __syncthreads();
-}
-
-// Persistent: the CTA takes the next `group` consecutive positions of the
-// permuted tile sequence per round (one per warp), then finishes their heavy
-// scalar ranges together, in position order.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async(DevLP L, StepParams P, PermKeys K, int64_t n_tiles,
-                                                               int group, int64_t heavy_limit,
-                                                               unsigned long long* next) {
+// Persistent, one warp = one worker: draw the next `batch` positions of the
+// permuted tile sequence (a stream = a contiguous part of the sequence; one
+// stream unless the grid is large) and process them.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async(DevLP L, StepParams P, AsyncCtx C, int batch,
+                                                               int64_t n_workers) {
     __shared__ WarpSmem wsm[kWarpsPerBlock];
-    __shared__ CtaSmem csm;
-    __shared__ int64_t heavy_tile[kWarpsPerBlock];
-    __shared__ int64_t base_s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (;;) {
-        // dynamic scheduling: positions are handed out in sequence order
-        if (threadIdx.x == 0) base_s = (int64_t)atomicAdd(next, (unsigned long long)group);
-        __syncthreads();
-        const int64_t base = base_s;
-        if (base >= n_tiles) break;
-        const int64_t t_idx = base + w;
-        bool heavy = false;
-        int64_t tile = -1;
-        if (w < group && t_idx < n_tiles) {
-            tile = (int64_t)tile_perm((uint64_t)t_idx, K);
-            heavy = async_tile_warp(L, P, tile, lane, wsm[w], heavy_limit);
+    WarpSmem& sm = wsm[w];
+    const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + w;
+    if (gw >= n_workers) return;
+    int st = (int)(gw % C.streams);
+    const int64_t per = (C.n_tiles + C.streams - 1) / C.streams;
+    for (int tries = 0; tries < C.streams;) {
+        const int64_t lo = st * per, hi = lo + per < C.n_tiles ? lo + per : C.n_tiles;
+        unsigned long long p0 = 0;
+        if (lane == 0) p0 = atomicAdd(C.next + st * 32, (unsigned long long)batch);
+        p0 = __shfl_sync(0xffffffffu, p0, 0);
+        const int64_t first = lo + (int64_t)p0;
+        if (first >= hi) { // this stream is exhausted: help the next one
+            st = (st + 1) % C.streams;
+            tries++;
+            continue;
         }
-        if (lane == 0) heavy_tile[w] = heavy ? tile : -1;
-        __syncthreads();
-        for (int h = 0; h < group; h++) {
-            const int64_t ht = heavy_tile[h];
-            if (ht >= 0) async_tile_cta(L, P, ht, csm);
+        // the batch's permuted tiles, one Feistel evaluation per lane
+        const int64_t mine = lane < batch && first + lane < hi ? (int64_t)tile_perm((uint64_t)(first + lane), C.K) : 0;
+        for (int i = 0; i < batch && first + i < hi; i++) {
+            const int64_t tile = __shfl_sync(0xffffffffu, mine, i);
+            process_tile(L, P, C, tile, sm, lane);
         }
-        __syncthreads();
+    }
+}
+
+__global__ void k_find_heavy(DevLP L, int64_t n_tiles, int64_t limit, int32_t* heavy, uint8_t* flags,
+                             unsigned long long* count) {
+    for (int64_t tile = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tile < n_tiles;
+         tile += (int64_t)gridDim.x * blockDim.x) {
+        int a, b;
+        scalar_lanes(L, tile * 32, a, b);
+        bool hv = false;
+        if (a < b) {
+            int64_t j0 = L.n_blocks * L.k + (tile * 32 + a - L.n_blocks);
+            hv = L.colptr[j0 + (b - a)] - L.colptr[j0] > limit;
+        }
+        flags[tile] = hv;
+        if (hv) heavy[atomicAdd(count, 1ull)] = (int32_t)tile;
     }
 }
 
@@ -515,11 +612,11 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 }
 
 // Bounded staleness (the async scheme needs the number of concurrent
-// updaters small relative to n): at most ~n_tiles / kAsyncDepth warps are in
-// flight (< 0.8% of the tiles), and never more than the device holds at once
-// (persistent grid); large LPs are bounded by the device, not by the depth.
+// updaters small relative to n): at most ~n_tiles / kAsyncDepth warps work at
+// once (< 0.8% of the tiles), and never more than the device holds (persistent
+// grid); large LPs are bounded by the device, not by the depth.
 constexpr int64_t kAsyncDepth = 128;
-static int64_t async_blocks(thetis_lp* lp, int64_t n_tiles) {
+static int64_t async_workers(int64_t n_tiles) {
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         int dev = 0;
@@ -528,11 +625,50 @@ static int64_t async_blocks(thetis_lp* lp, int64_t n_tiles) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async, kWarpsPerBlock * 32, 0);
         if (per_sm < 1) per_sm = 1;
     }
-    (void)lp;
-    int64_t depth_cap = (n_tiles + kWarpsPerBlock * kAsyncDepth - 1) / (kWarpsPerBlock * kAsyncDepth);
-    int64_t dev_cap = (int64_t)per_sm * sms;
-    int64_t b = depth_cap < dev_cap ? depth_cap : dev_cap;
-    return b < 1 ? 1 : b;
+    int64_t depth_cap = n_tiles / kAsyncDepth;
+    int64_t dev_cap = (int64_t)per_sm * sms * kWarpsPerBlock;
+    int64_t w = depth_cap < dev_cap ? depth_cap : dev_cap;
+    return w < 1 ? 1 : w;
+}
+
+// hub tiles (VC / MIS only, see the hub step): per-tile flags and the sorted
+// list, cached per LP in the persistent `heavy` region (8 n_tiles + 8 bytes:
+// flags in the first n_tiles bytes, then the list)
+static bool hub_step_enabled(const DevLP& L) {
+    return L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS;
+}
+static uint8_t* hub_flags(thetis_lp* lp) { return (uint8_t*)lp->heavy; }
+static int64_t struct_tiles(const DevLP& L) { return (L.n_blocks + L.n_scalar + 31) / 32; }
+static int32_t* hub_list(thetis_lp* lp) {
+    const int64_t n_tiles = struct_tiles(lp->d);
+    return lp->heavy + (n_tiles + 3) / 4;
+}
+static int ensure_heavy(thetis_lp* lp) {
+    if (lp->heavy_valid) return THETIS_OK;
+    const DevLP& L = lp->d;
+    cudaStream_t s = lp->stream;
+    const int64_t n_tiles = struct_tiles(L);
+    lp->n_heavy = 0;
+    if (hub_step_enabled(L) && n_tiles > 0) {
+        Carver C(lp->temp);
+        int32_t* unsorted = C.take<int32_t>(n_tiles);
+        unsigned long long* cnt = C.take<unsigned long long>(1);
+        CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
+        k_find_heavy<<<grid_for(n_tiles, 256), 256, 0, s>>>(L, n_tiles, kHeavy, unsorted, hub_flags(lp), cnt);
+        unsigned long long h = 0;
+        CUDA_TRY(lp, cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        lp->n_heavy = (int64_t)h;
+        if (h > 0) {
+            size_t cb = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, cb, unsorted, hub_list(lp), (int64_t)h, 0, 32);
+            void* cubp = C.take<char>((int64_t)cb);
+            if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "heavy list temp");
+            CUDA_TRY(lp, cub::DeviceRadixSort::SortKeys(cubp, cb, unsorted, hub_list(lp), (int64_t)h, 0, 32, s));
+        }
+    }
+    lp->heavy_valid = true;
+    return check_cuda(lp, "heavy tiles");
 }
 
 int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
@@ -546,6 +682,29 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     const double Lmax = (double)beta * lp->maxnorm2 + 1.0 / (double)beta; // Eq. 7
     P.invLmax = (float)(1.0 / Lmax);
     if (mode == THETIS_MODE_DETERMINISTIC) THETIS_TRY(ensure_colouring(lp, seed));
+    const int64_t n_tiles = struct_tiles(L); // (3) permutes the tiles of structural units
+    const bool serial = mode == THETIS_MODE_ASYNC_SERIAL;
+    AsyncCtx AC{};
+    HubCtx H{};
+    int64_t blocks = 1, hub_blocks = 1, workers = 1;
+    int batch = 1;
+    if (mode != THETIS_MODE_DETERMINISTIC) {
+        THETIS_TRY(ensure_heavy(lp));
+        H.n_heavy = lp->n_heavy;
+        H.heavy_tiles = hub_list(lp);
+        H.hub_tile = hub_flags(lp);
+        workers = serial ? 1 : async_workers(n_tiles);
+        blocks = (workers + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        AC.streams = blocks >= 128 ? (int)(blocks / 64) : 1;
+        batch = blocks >= 128 ? kBatch : 1;
+        Carver C(lp->temp);
+        AC.next = C.take<unsigned long long>(32 * (int64_t)AC.streams);
+        H.buf = C.take<float>(H.n_heavy > 0 ? L.n_s : 1);
+        if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
+        AC.n_tiles = n_tiles;
+        AC.heavy_limit = hub_step_enabled(L) ? kHeavy : INT64_MAX;
+        hub_blocks = grid_for(L.m, 256, 148 * 8);
+    }
     const bool timed = st != nullptr;
     if (timed) {
         if (lp->ev_epoch.empty()) {
@@ -553,7 +712,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             for (auto& e : lp->ev_epoch) CUDA_TRY(lp, cudaEventCreate(&e));
         }
     }
-    const int64_t n_tiles = (L.U + 31) / 32;
     cudaEvent_t ev_start = timed ? lp->ev_epoch[0] : nullptr;
     if (timed) CUDA_TRY(lp, cudaEventRecord(ev_start, s));
     for (int e = 0; e < epochs; e++) {
@@ -564,14 +722,21 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             }
             if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, s>>>(L, P);
         } else {
-            PermKeys K = make_perm_keys(n_tiles, seed, e);
+            // (1) hub step + (2) slack sweep, fused; or (2) alone
+            if (H.n_heavy > 0) {
+                const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
+                k_zero_hub_buf<<<hb, 256, 0, s>>>(H);
+                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H);
+                k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
+                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H);
+            } else if (L.n_ineq > 0) {
+                k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
+            }
+            // (3) the permuted tiles of structural units
             if (n_tiles > 0) {
-                const bool serial = mode == THETIS_MODE_ASYNC_SERIAL;
-                int64_t blocks = serial ? 1 : async_blocks(lp, n_tiles);
-                unsigned long long* next = (unsigned long long*)(lp->flags + 56);
-                CUDA_TRY(lp, cudaMemsetAsync(next, 0, 8, s));
-                k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, K, n_tiles,
-                                                                         serial ? 1 : kWarpsPerBlock, kHeavy, next);
+                CUDA_TRY(lp, cudaMemsetAsync(AC.next, 0, (size_t)AC.streams * 32 * 8, s));
+                AC.K = make_perm_keys(n_tiles, seed, e);
+                k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));

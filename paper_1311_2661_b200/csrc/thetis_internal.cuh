@@ -188,6 +188,7 @@ struct thetis_lp {
     // heavy tile list (async)
     bool heavy_valid = false;
     int64_t n_heavy = 0;
+    int64_t n_hub_chunks = 0;
     bool anchors = false;
     char err[512] = {0};
 };

@@ -267,7 +267,7 @@ def test_graph_encoding_counts():
     lp = RefLP.graph(VC, 30, src, dst, vertex_w=w)
     assert lp.m == len(edges) and lp.nnz_struct == 2 * len(edges) and lp.n_ineq == len(edges)
     eu, ev = lp.edges()
-    assert list(zip(eu.tolist(), ev.tolist())) == edges
+    assert list(zip(eu.tolist(), ev.tolist())) == sorted(edges, key=lambda e: (e[1], e[0]))
     b, sense, c = lp.rows()
     assert (b == 1).all() and (sense == oracle.SENSE_GE).all()
     lpm = RefLP.graph(MIS, 30, src, dst, vertex_w=w)
