@@ -411,67 +411,74 @@ __device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P
 struct HubCtx {
     int64_t n_heavy;
     const int32_t* heavy_tiles;  // sorted tile ids
-    const uint8_t* hub_tile;     // per tile: 1 if hub tile
-    float* buf;                  // per vertex: partial dot, then step (hub vertices only)
+    const int32_t* hub_id;       // per structural tile: index in heavy_tiles, or -1
+    const int2* row_slot;        // per row: accumulator slots of (min, max) endpoint, -1 if not a hub
+    float* buf;                  // compact accumulators, transposed: [lane][hub id] (L2-resident,
+                                 // and the top hubs 0, 1, 2, 4, ... fall in different lines)
 };
-__device__ __forceinline__ bool is_hub(const HubCtx& H, int32_t v) { return H.hub_tile[v >> 5] != 0; }
+__device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int64_t v) {
+    const int32_t h = H.hub_id[v >> 5];
+    return h < 0 ? -1 : (int32_t)((v & 31) * H.n_heavy + h);
+}
 
-// the accumulators of vertices below kPriv (where the natural-id power-law
-// generators put their biggest hubs) are privatised per CTA in shared memory:
-// the top hubs take ~1e6 additions per epoch, too many for one L2 address
-constexpr int kPriv = 8192;
+__global__ void k_hub_ids(int64_t n_heavy, const int32_t* heavy_tiles, int32_t* hub_id) {
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n_heavy; h += (int64_t)gridDim.x * blockDim.x)
+        hub_id[heavy_tiles[h]] = (int32_t)h;
+}
+__global__ void k_row_slots(DevLP L, HubCtx H, int2* row_slot) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int2 uv = L.edges[e];
+        row_slot[e] = make_int2(hub_slot(H, uv.x), hub_slot(H, uv.y));
+    }
+}
+
+constexpr int kRowsPerThread = 4;
+// (1a) r_e into the accumulators of the hub endpoints: the min endpoint by an
+// atomic per row, the max endpoint (rows come in runs of equal max endpoint, so
+// of equal slot) by a segmented warp sum and one atomic per run segment.
+// kRowsPerThread rows per thread, all loads issued before any atomic.
 __global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H) {
-    __shared__ float priv[kPriv];
-    for (int i = threadIdx.x; i < kPriv; i += blockDim.x) priv[i] = 0.0f;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e - lane < L.m; e += stride) {
-        int2 uv = make_int2(0, 0);
-        float rv = 0.0f;
-        bool hu = false, hv = false;
-        if (e < L.m) {
-            uv = L.edges[e];
-            hu = is_hub(H, uv.x);
-            hv = is_hub(H, uv.y);
-            if (hu || hv) rv = L.r[e];
-        }
-        if (hu) {
-            if (uv.x < kPriv) atomicAdd(priv + uv.x, rv);
-            else atomicAdd(H.buf + uv.x, rv);
-        }
-        // rows come in runs of equal max endpoint v (hub-ness is constant on a
-        // run): segmented suffix sums over the warp, one addition per run segment
-        float sv = hv ? rv : 0.0f;
-        const int key = hv ? uv.y : -1;
+    const int64_t span = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
+         e0 += kRowsPerThread * span) {
+        int2 sl[kRowsPerThread];
+        float rv[kRowsPerThread];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const float x = __shfl_down_sync(0xffffffffu, sv, o);
-            const int k2 = __shfl_down_sync(0xffffffffu, key, o);
-            if (lane + o < 32 && k2 == key) sv += x;
+        for (int q = 0; q < kRowsPerThread; q++) {
+            const int64_t e = e0 + q * span;
+            sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
+            rv[q] = e < L.m ? ld_cg(L.r + e) : 0.0f;
         }
-        const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-        if (hv && (lane == 0 || prev != key)) {
-            if (uv.y < kPriv) atomicAdd(priv + uv.y, sv);
-            else atomicAdd(H.buf + uv.y, sv);
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; q++) {
+            if (sl[q].x >= 0) atomicAdd(H.buf + sl[q].x, rv[q]);
+            float sv = sl[q].y >= 0 ? rv[q] : 0.0f;
+            const int key = sl[q].y;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float x = __shfl_down_sync(0xffffffffu, sv, o);
+                const int k2 = __shfl_down_sync(0xffffffffu, key, o);
+                if (lane + o < 32 && k2 == key) sv += x;
+            }
+            const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+            if (key >= 0 && (lane == 0 || prev != key)) atomicAdd(H.buf + key, sv);
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kPriv; i += blockDim.x)
-        if (priv[i] != 0.0f) atomicAdd(H.buf + i, priv[i]);
 }
 // the hub steps: buf[j] holds D_j on entry and the step d_j on exit
 __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= H.n_heavy * 32) return;
-    const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
+    const int64_t h = i % H.n_heavy, lane = i / H.n_heavy; // slot i = lane * n_heavy + h
+    const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
     if (j >= L.n_scalar) return;
     float z = L.z[j];
-    float g = grad_from(c_int(L, j), ua_of(L, j), H.buf[j], z, zbar_of(L, j), P.beta);
+    float g = grad_from(c_int(L, j), ua_of(L, j), H.buf[i], z, zbar_of(L, j), P.beta);
     float invL = unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
-    H.buf[j] = __fsub_rn(zn, z);
+    H.buf[i] = __fsub_rn(zn, z);
 }
 // (2) fused with the end of (1): per row, add the hub steps of both endpoints to
 // r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has
@@ -479,10 +486,10 @@ __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
 __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += stride) {
-        const int2 uv = L.edges[e];
+        const int2 sl = H.row_slot[e];
         float delta = 0.0f;
-        if (is_hub(H, uv.x)) delta = H.buf[uv.x];
-        if (is_hub(H, uv.y)) delta = __fadd_rn(delta, H.buf[uv.y]);
+        if (sl.x >= 0) delta = H.buf[sl.x];
+        if (sl.y >= 0) delta = __fadd_rn(delta, H.buf[sl.y]);
         const float r0 = L.r[e];
         float rv = delta != 0.0f ? __fadd_rn(r0, delta) : r0;
         const int64_t j = L.n_s + e;
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(256) k_slack_sweep(DevLP L, StepParams P) {
 }
 __global__ void k_zero_hub_buf(HubCtx H) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < H.n_heavy * 32) H.buf[(int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31)] = 0.0f;
+    if (i < H.n_heavy * 32) H.buf[i] = 0.0f;
 }
 
 struct AsyncCtx {
@@ -692,15 +699,23 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         THETIS_TRY(ensure_heavy(lp));
         H.n_heavy = lp->n_heavy;
         H.heavy_tiles = hub_list(lp);
-        H.hub_tile = hub_flags(lp);
         workers = serial ? 1 : async_workers(n_tiles);
         blocks = (workers + kWarpsPerBlock - 1) / kWarpsPerBlock;
         AC.streams = blocks >= 128 ? (int)(blocks / 64) : 1;
         batch = blocks >= 128 ? kBatch : 1;
         Carver C(lp->temp);
         AC.next = C.take<unsigned long long>(32 * (int64_t)AC.streams);
-        H.buf = C.take<float>(H.n_heavy > 0 ? L.n_s : 1);
+        int2* row_slot = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
+        int32_t* hub_id = C.take<int32_t>(n_tiles);
+        H.row_slot = row_slot;
+        H.hub_id = hub_id;
+        H.buf = C.take<float>(H.n_heavy * 32);
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
+        if (H.n_heavy > 0) {
+            CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
+            k_hub_ids<<<grid_for(H.n_heavy, 256), 256, 0, s>>>(H.n_heavy, H.heavy_tiles, hub_id);
+            k_row_slots<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, row_slot);
+        }
         AC.n_tiles = n_tiles;
         AC.heavy_limit = hub_step_enabled(L) ? kHeavy : INT64_MAX;
         hub_blocks = grid_for(L.m, 256, 148 * 8);
