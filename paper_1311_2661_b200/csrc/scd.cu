@@ -433,11 +433,35 @@ __global__ void k_row_slots(DevLP L, HubCtx H, int2* row_slot) {
 }
 
 constexpr int kRowsPerThread = 4;
+
+// v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
+// not a hub); add the warp's run segments with one atomic each.  Fast path when
+// the whole warp is one run.
+__device__ __forceinline__ void add_max_side(float* acc, int key, float val, int lane) {
+    const int k0 = __shfl_sync(0xffffffffu, key, 0);
+    if (__all_sync(0xffffffffu, key == k0)) {
+        if (k0 < 0) return;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        if (lane == 0) atomicAdd(acc + k0, val);
+        return;
+    }
+    float sv = key >= 0 ? val : 0.0f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float x = __shfl_down_sync(0xffffffffu, sv, o);
+        const int k2 = __shfl_down_sync(0xffffffffu, key, o);
+        if (lane + o < 32 && k2 == key) sv += x;
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    if (key >= 0 && (lane == 0 || prev != key)) atomicAdd(acc + key, sv);
+}
 // (1a) r_e into the accumulators of the hub endpoints: the min endpoint by an
-// atomic per row, the max endpoint (rows come in runs of equal max endpoint, so
-// of equal slot) by a segmented warp sum and one atomic per run segment.
-// kRowsPerThread rows per thread, all loads issued before any atomic.
-__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H) {
+// atomic per row, the max endpoint by add_max_side.  kRowsPerThread rows per
+// thread, all loads issued before any atomic.  With light_only, rows whose
+// endpoints are both hubs are skipped: the previous epoch's row pass already
+// added their (since unchanged) r_e.
+__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, float* acc, int light_only) {
     const int lane = threadIdx.x & 31;
     const int64_t span = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
@@ -448,21 +472,13 @@ __global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H) {
         for (int q = 0; q < kRowsPerThread; q++) {
             const int64_t e = e0 + q * span;
             sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
-            rv[q] = e < L.m ? ld_cg(L.r + e) : 0.0f;
+            if (light_only && sl[q].x >= 0 && sl[q].y >= 0) sl[q] = make_int2(-1, -1);
+            rv[q] = (sl[q].x >= 0 || sl[q].y >= 0) ? ld_cg(L.r + e) : 0.0f;
         }
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
-            if (sl[q].x >= 0) atomicAdd(H.buf + sl[q].x, rv[q]);
-            float sv = sl[q].y >= 0 ? rv[q] : 0.0f;
-            const int key = sl[q].y;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const float x = __shfl_down_sync(0xffffffffu, sv, o);
-                const int k2 = __shfl_down_sync(0xffffffffu, key, o);
-                if (lane + o < 32 && k2 == key) sv += x;
-            }
-            const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-            if (key >= 0 && (lane == 0 || prev != key)) atomicAdd(H.buf + key, sv);
+            if (sl[q].x >= 0) atomicAdd(acc + sl[q].x, rv[q]);
+            add_max_side(acc, sl[q].y, rv[q], lane);
         }
     }
 }
@@ -483,33 +499,57 @@ __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
 // (2) fused with the end of (1): per row, add the hub steps of both endpoints to
 // r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has
 // slack column n + e); one read-modify-write of r and s per row
-__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += stride) {
-        const int2 sl = H.row_slot[e];
-        float delta = 0.0f;
-        if (sl.x >= 0) delta = H.buf[sl.x];
-        if (sl.y >= 0) delta = __fadd_rn(delta, H.buf[sl.y]);
-        const float r0 = L.r[e];
-        float rv = delta != 0.0f ? __fadd_rn(r0, delta) : r0;
-        const int64_t j = L.n_s + e;
-        const float sig = row_sigma(L, e);
-        const float z = L.z[j];
-        const float zn = slack_new(L, P, e, j, sig, rv, z);
-        const float d = __fsub_rn(zn, z);
-        if (d != 0.0f) rv = __fadd_rn(rv, sig < 0.0f ? -d : d);
-        if (rv != r0) L.r[e] = rv;
-        if (d != 0.0f) L.z[j] = zn;
+__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H, float* acc_next) {
+    const int lane = threadIdx.x & 31;
+    const int64_t span = (int64_t)gridDim.x * blockDim.x;
+    const bool lmax = P.rule == THETIS_STEP_LMAX;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
+         e0 += kRowsPerThread * span) {
+        int2 sl[kRowsPerThread];
+        float r0[kRowsPerThread], z[kRowsPerThread];
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; q++) {
+            const int64_t e = e0 + q * span;
+            const bool ok = e < L.m;
+            sl[q] = ok ? H.row_slot[e] : make_int2(-1, -1);
+            r0[q] = ok ? L.r[e] : 0.0f;
+            z[q] = ok ? L.z[L.n_s + e] : 0.0f;
+        }
+        float rv[kRowsPerThread];
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; q++) {
+            const int64_t e = e0 + q * span;
+            float delta = 0.0f;
+            if (sl[q].x >= 0) delta = H.buf[sl[q].x];
+            if (sl[q].y >= 0) delta = __fadd_rn(delta, H.buf[sl[q].y]);
+            rv[q] = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
+            if (e < L.m) {
+                const int64_t j = L.n_s + e;
+                const float sig = row_sigma(L, e);
+                const float zn = slack_new(L, P, e, j, sig, rv[q], z[q]);
+                const float d = __fsub_rn(zn, z[q]);
+                if (d != 0.0f) {
+                    rv[q] = __fadd_rn(rv[q], sig < 0.0f ? -d : d);
+                    L.z[j] = zn;
+                }
+                if (rv[q] != r0[q]) L.r[e] = rv[q];
+            }
+        }
+        (void)lmax;
+        // a hub-hub row is not touched again before the next epoch's hub step:
+        // add its final r_e to the next epoch's accumulators now
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; q++) {
+            const bool hh = sl[q].x >= 0 && sl[q].y >= 0;
+            if (hh) atomicAdd(acc_next + sl[q].x, rv[q]);
+            add_max_side(acc_next, hh ? sl[q].y : -1, rv[q], lane);
+        }
     }
 }
 // (2) without a hub step: the slack sweep
 __global__ void __launch_bounds__(256) k_slack_sweep(DevLP L, StepParams P) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L.n_ineq; q += (int64_t)gridDim.x * blockDim.x)
         update_slack(L, P, q);
-}
-__global__ void k_zero_hub_buf(HubCtx H) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < H.n_heavy * 32) H.buf[i] = 0.0f;
 }
 
 struct AsyncCtx {
@@ -694,6 +734,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     AsyncCtx AC{};
     HubCtx H{};
     int64_t blocks = 1, hub_blocks = 1, workers = 1;
+    float* hub_acc[2] = {nullptr, nullptr};
     int batch = 1;
     if (mode != THETIS_MODE_DETERMINISTIC) {
         THETIS_TRY(ensure_heavy(lp));
@@ -709,7 +750,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         int32_t* hub_id = C.take<int32_t>(n_tiles);
         H.row_slot = row_slot;
         H.hub_id = hub_id;
-        H.buf = C.take<float>(H.n_heavy * 32);
+        hub_acc[0] = C.take<float>(H.n_heavy * 32);
+        hub_acc[1] = C.take<float>(H.n_heavy * 32);
+        H.buf = hub_acc[0];
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
         if (H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
@@ -739,11 +782,16 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         } else {
             // (1) hub step + (2) slack sweep, fused; or (2) alone
             if (H.n_heavy > 0) {
+                // accumulators ping-pong: the hub-hub part of this epoch's D was added
+                // by the previous epoch's row pass (except in a solve's first epoch)
                 const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
-                k_zero_hub_buf<<<hb, 256, 0, s>>>(H);
-                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H);
+                float* acc_next = H.buf == hub_acc[0] ? hub_acc[1] : hub_acc[0];
+                if (e == 0) CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
+                CUDA_TRY(lp, cudaMemsetAsync(acc_next, 0, (size_t)H.n_heavy * 32 * 4, s));
+                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf, e == 0 ? 0 : 1);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
-                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H);
+                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H, acc_next);
+                H.buf = acc_next;
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
             }
