@@ -77,11 +77,12 @@ def algorithmic_bytes(n_s, nnz_s, m):
 
 
 def ncu_traffic():
-    """dram bytes per launch of the async kernel from the committed ncu summary, or None"""
+    """DRAM bytes of one SCD epoch (its kernels' dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed ncu summary (tools/profile_round.sh + tools/ncu_summary.py), or None"""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get("k_async_dram_bytes_per_launch")
+            return json.load(f).get("epoch_dram_bytes")
     except Exception:
         return None
 
@@ -297,7 +298,9 @@ def run_thetis(args):
                   "nnz_per_s": nnz_step / EPOCHS / (ep_med / 1e3), "alg_bytes": b_epoch,
                   "GBps": achieved, "frac_of_8TBps_nominal": achieved / 8000.0},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(), "kernel": "k_async (one launch = one epoch)", "peak_source": peak_src},
+                     "traffic": ncu_traffic(),
+                     "kernel": "one SCD epoch = k_hub_rows_gather + k_hub_update + k_rows_hub_slack + k_async "
+                               "(CUDA events around each epoch on the launching stream)", "peak_source": peak_src},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),
                    "selected": int(rr.n_selected)},

@@ -49,6 +49,12 @@ __device__ __forceinline__ float ld_cg(const float* p) {
     asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
 }
+// streaming load of CSC indices (read once per pass; do not keep in L1)
+__device__ __forceinline__ int32_t ld_cs_i32(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
@@ -323,42 +329,50 @@ __device__ __forceinline__ int col_of(const WarpSmem& sm, int ncols, int64_t t) 
     }
     return lo;
 }
-__device__ __forceinline__ float nz_value(const DevLP& L, int64_t t) {
-    int64_t row;
-    float av;
-    entry(L, t, row, av);
-    float rv = ld_cg(L.r + row);
-    return L.val ? av * rv : (av < 0.0f ? -rv : rv);
-}
-__device__ __forceinline__ void nz_scatter(const DevLP& L, int64_t t, float d) {
-    int64_t row;
-    float av;
-    entry(L, t, row, av);
-    red_add(L.r + row, L.val ? av * d : (av < 0.0f ? -d : d));
-}
-
 // partial dots of the tile's columns over the nonzero range [c0, c1), added into
 // sm.acc.  Sub-chunks of 32 lying inside one column accumulate in registers;
 // mixed sub-chunks locate each lane's column and add with shared atomics.
 __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
                                              int lane) {
+    constexpr int U = 4; // sub-chunks in flight: their loads are issued before any use
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
     float acc = 0.0f;
-    for (int64_t base = c0; base < c1; base += 32) {
-        if (nb <= base) {
-            acc = warp_sum(acc);
-            if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
-            acc = 0.0f;
-            do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
+        uint32_t raw[U];
+        float v[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t t = b0 + 32 * q + lane;
+            raw[q] = t < c1 ? (uint32_t)L.rowidx[t] : 0u;  // re-read by the scatter: keep cached
         }
-        const int64_t t = base + lane;
-        if (base + 32 <= nb || c1 <= nb) {
-            if (t < c1) acc += nz_value(L, t);
-        } else if (t < c1) {
-            int col = c;
-            while (sm.cp[col + 1] <= t) col++;
-            atomicAdd(&sm.acc[col], nz_value(L, t));
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t t = b0 + 32 * q + lane;
+            v[q] = 0.0f;
+            if (t < c1) {
+                const float rv = ld_cg(L.r + (raw[q] & kRowMask));
+                v[q] = L.val ? L.val[t] * rv : ((raw[q] & kSignBit) ? -rv : rv);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t base = b0 + 32 * q;
+            if (base >= c1) break;
+            if (nb <= base) {
+                acc = warp_sum(acc);
+                if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
+                acc = 0.0f;
+                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+            }
+            const int64_t t = base + lane;
+            if (base + 32 <= nb || c1 <= nb) {
+                acc += v[q];
+            } else if (t < c1) {
+                int col = c;
+                while (sm.cp[col + 1] <= t) col++;
+                atomicAdd(&sm.acc[col], v[q]);
+            }
         }
     }
     acc = warp_sum(acc);
@@ -368,22 +382,36 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
 // r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]
 __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
                                               int lane) {
+    constexpr int U = 4;
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
     float dc = sm.d[c];
-    for (int64_t base = c0; base < c1; base += 32) {
-        if (nb <= base) {
-            do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
-            dc = sm.d[c];
+    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
+        uint32_t raw[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t t = b0 + 32 * q + lane;
+            raw[q] = t < c1 ? (uint32_t)ld_cs_i32(L.rowidx + t) : 0u;
         }
-        const int64_t t = base + lane;
-        if (base + 32 <= nb || c1 <= nb) {
-            if (t < c1 && dc != 0.0f) nz_scatter(L, t, dc);
-        } else if (t < c1) {
-            int col = c;
-            while (sm.cp[col + 1] <= t) col++;
-            const float d = sm.d[col];
-            if (d != 0.0f) nz_scatter(L, t, d);
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t base = b0 + 32 * q;
+            if (base >= c1) break;
+            if (nb <= base) {
+                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+                dc = sm.d[c];
+            }
+            const int64_t t = base + lane;
+            float d = dc;
+            if (!(base + 32 <= nb || c1 <= nb) && t < c1) {
+                int col = c;
+                while (sm.cp[col + 1] <= t) col++;
+                d = sm.d[col];
+            }
+            if (t < c1 && d != 0.0f) {
+                const float a = L.val ? L.val[t] : ((raw[q] & kSignBit) ? -1.0f : 1.0f);
+                red_add(L.r + (raw[q] & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
+            }
         }
     }
 }
