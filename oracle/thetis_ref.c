@@ -634,15 +634,19 @@ int thetis_ref_step_unit(ref_lp* lp, float beta, int64_t u, int step_rule) {
 /* ------------------------------------------------------------------ */
 /* sweep orders (R-5, R-6)                                   */
 /* ------------------------------------------------------------------ */
-typedef struct { uint32_t prio; int64_t id; } prio_unit;
+/* priority order of the colouring (R-5): more nonzeros first (largest degree
+ * first), then the larger hash, then the smaller id */
+typedef struct { int64_t deg; uint32_t prio; int64_t id; } prio_unit;
 static int cmp_prio(const void* a, const void* b) {
     const prio_unit* x = (const prio_unit*)a;
     const prio_unit* y = (const prio_unit*)b;
+    if (x->deg != y->deg) return x->deg > y->deg ? -1 : 1;
     if (x->prio != y->prio) return x->prio > y->prio ? -1 : 1;
     return x->id < y->id ? -1 : (x->id > y->id);
 }
 
-/* Sequential greedy colouring in priority order: colour(u) = smallest colour
+/* Sequential greedy colouring in priority order (largest degree first, R-5):
+ * colour(u) = smallest colour
  * not used by an already-coloured unit that shares a row of A with u.
  * Only non-fixed structural units take part; slacks form class K. */
 int64_t thetis_ref_colouring(ref_lp* lp, uint64_t seed, int32_t* colour) {
@@ -670,6 +674,10 @@ int64_t thetis_ref_colouring(ref_lp* lp, uint64_t seed, int32_t* colour) {
     for (int64_t u = 0; u < S; u++) {
         colour[u] = -1;
         if (unit_fixed(lp, u)) continue;
+        int64_t f, c, deg = 0;
+        unit_cols(lp, u, &f, &c);
+        for (int64_t j = f; j < f + c; j++) deg += col_nnz(lp, j);
+        order[cnt].deg = deg;
         order[cnt].prio = fmix32((uint32_t)u ^ key);
         order[cnt].id = u;
         cnt++;

@@ -370,7 +370,8 @@ size_t post_build_temp(int64_t S, int64_t n_struct, int64_t n_vert) {
     cub::DeviceRadixSort::SortPairs(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, S, 0, 32);
     mx = b;
-    size_t colour = 2 * 256 + 2 * (size_t)S * 4 + mx + 4 * 256;
+    // colouring: keys, ids, sorted keys, class start / end (<= S + 2 each), CUB temp
+    size_t colour = 8 * 256 + 5 * ((size_t)S + 2) * 4 + mx + 4 * 256;
     size_t round = 8 * 256 + (size_t)n_struct * 4 + 2 * (size_t)n_vert + (size_t)64 * kRedBlocks * 8 + 64 * 8 + 64 + 32;
     return colour > round ? colour : round;
 }

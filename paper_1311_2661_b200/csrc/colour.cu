@@ -4,8 +4,9 @@
 // takes the smallest colour none of them uses.  A unit is coloured exactly when
 // all units preceding it in priority order among its neighbours are, so the
 // result equals the sequential first-fit greedy in priority order.
-// Priorities: prio(u) = fmix32(u ^ key), key = fmix32(lo32 seed) ^ hi32 seed,
-// ties (impossible: fmix32 is a bijection) broken by the smaller id.
+// Priorities (R-5): largest degree (nonzeros of the unit's columns) first, then
+// fmix32(u ^ key), key = fmix32(lo32 seed) ^ hi32 seed, then the smaller id.
+// Largest-degree-first colours power-law hubs in the first rounds.
 #include <cub/cub.cuh>
 
 #include "thetis_internal.cuh"
@@ -19,8 +20,19 @@ __device__ __forceinline__ int64_t unit_of_col(const DevLP& L, int64_t j) {
     const int64_t nbk = L.n_blocks * L.k;
     return j < nbk ? j / L.k : L.n_blocks + (j - nbk);
 }
-__device__ __forceinline__ bool precedes(uint32_t pw, int64_t w, uint32_t pu, int64_t u) {
-    return pw > pu || (pw == pu && w < u);
+// rank(u) = (nonzeros of u's columns << 32) | fmix32(u ^ key): largest degree
+// first, then the larger hash; equal ranks (impossible for distinct hashes) by id
+__device__ __forceinline__ bool precedes(uint64_t rw, int64_t w, uint64_t ru, int64_t u) {
+    return rw > ru || (rw == ru && w < u);
+}
+__global__ void k_colour_rank(DevLP L, int64_t S, uint32_t key, uint64_t* rank) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
+        int64_t first, cnt;
+        if (u < L.n_blocks) { first = u * L.k; cnt = L.k; }
+        else { first = L.n_blocks * L.k + (u - L.n_blocks); cnt = 1; }
+        const uint64_t deg = (uint64_t)(L.colptr[first + cnt] - L.colptr[first]);
+        rank[u] = (deg << 32) | fmix32((uint32_t)u ^ key);
+    }
 }
 
 // visit the conflict neighbours of unit u (units sharing a row), f(w) returns
@@ -60,18 +72,18 @@ __global__ void k_colour_init(DevLP L, int64_t S, int32_t* colour) {
         colour[u] = (L.unit_fixed && L.unit_fixed[u]) ? -2 : -1;
 }
 
-__global__ void k_jp_round(DevLP L, int64_t S, uint32_t key, int32_t* colour, unsigned long long* remaining) {
+__global__ void k_jp_round(DevLP L, int64_t S, const uint64_t* __restrict__ rank, int32_t* colour,
+                           unsigned long long* remaining) {
     unsigned long long left = 0;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
         if (colour[u] != -1) continue;
-        const uint32_t pu = fmix32((uint32_t)u ^ key);
+        const uint64_t pu = rank[u];
         int32_t base = 0;
         bool ready = true, done = false;
         while (!done) {
             unsigned long long mask = 0;
             for_each_neighbour(L, u, [&](int64_t w) {
-                uint32_t pw = fmix32((uint32_t)w ^ key);
-                if (!precedes(pw, w, pu, u)) return true;
+                if (!precedes(rank[w], w, pu, u)) return true;
                 int32_t cw = ((volatile int32_t*)colour)[w];
                 if (cw == -2) return true;
                 if (cw == -1) { ready = false; return false; }
@@ -130,10 +142,13 @@ int ensure_colouring(thetis_lp* lp, uint64_t seed) {
     int32_t K = 0;
     if (S > 0) {
         unsigned long long* remaining = (unsigned long long*)(lp->flags + 32);
+        uint64_t* rank = (uint64_t*)lp->temp;
+        if ((size_t)S * 8 > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "colouring ranks");
+        k_colour_rank<<<grid_for(S, T), T, 0, s>>>(L, S, key, rank);
         k_colour_init<<<grid_for(S, T), T, 0, s>>>(L, S, lp->colour);
         for (int round = 0;; round++) {
             CUDA_TRY(lp, cudaMemsetAsync(remaining, 0, 8, s));
-            k_jp_round<<<grid_for(S, T), T, 0, s>>>(L, S, key, lp->colour, remaining);
+            k_jp_round<<<grid_for(S, T), T, 0, s>>>(L, S, rank, lp->colour, remaining);
             unsigned long long left = 0;
             CUDA_TRY(lp, cudaMemcpyAsync(&left, remaining, 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));

@@ -367,7 +367,8 @@ def _fmix32(h):
 @pytest.mark.parametrize("problem", [VC, MWC])
 def test_colouring_is_proper_and_first_fit(problem):
     # definition (R-5): proper (no two units of a class share a row) and first-fit in
-    # priority order: colour(u) = mex of the colours of higher-priority conflicting units
+    # priority order (largest degree first): colour(u) = mex of the colours of the
+    # higher-priority conflicting units
     src, dst = small_graph(40, 120, 12)
     if problem == VC:
         lp = RefLP.graph(VC, 40, src, dst, vertex_w=np.ones(40, np.float32))
@@ -379,7 +380,15 @@ def test_colouring_is_proper_and_first_fit(problem):
     rows = _unit_rows(lp)
     S = len(rows)
     key = _fmix32(seed & 0xFFFFFFFF) ^ (seed >> 32)
-    prio = [_fmix32(u ^ key) for u in range(S)]
+    cp, _, _ = lp.csc()
+    k = max(lp.block_k, 1)
+
+    def deg(u):
+        cols = range(u * k, u * k + k) if u < lp.n_blocks else [lp.n_blocks * lp.block_k + u - lp.n_blocks]
+        return sum(int(cp[j + 1] - cp[j]) for j in cols)
+
+    # priority: largest degree first, then the larger hash, then the smaller id
+    prio = [(deg(u), _fmix32(u ^ key)) for u in range(S)]
     assert (col[S:] == K).all()
     for u in range(S):
         if col[u] < 0:
