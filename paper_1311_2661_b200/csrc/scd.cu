@@ -38,7 +38,7 @@ constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the war
 
 struct StepParams {
     float beta;       // caller's beta
-    float inv_beta_unused;
+    float inv_beta;   // fl(1 / beta), async kernels only
     float invLmax;    // (float)(1 / L_max), L_max in fp64 (Eq. 7)
     double beta_d;    // (double)beta
     int rule;         // THETIS_STEP_LMAX / THETIS_STEP_LJ
@@ -64,11 +64,19 @@ __device__ __forceinline__ float unit_invL(const StepParams& P, double norm2) {
     return (float)(1.0 / (P.beta_d * norm2 + 1.0 / P.beta_d));
 }
 
-// g = c - ua + beta D + (z - zbar)/beta, each operation rounded on its own
+// g = c - ua + beta D + (z - zbar)/beta, each operation rounded on its own (the
+// deterministic contract); the async kernels (not bit-exact by nature) multiply
+// by inv_beta = fl(1/beta) instead of dividing
 __device__ __forceinline__ float grad_from(float c, float ua, float D, float z, float zb, float beta) {
     float g = __fsub_rn(c, ua);
     g = __fadd_rn(g, __fmul_rn(beta, D));
     g = __fadd_rn(g, __fdiv_rn(__fsub_rn(z, zb), beta));
+    return g;
+}
+__device__ __forceinline__ float grad_fast(float c, float ua, float D, float z, float zb, float beta, float inv_beta) {
+    float g = __fsub_rn(c, ua);
+    g = __fadd_rn(g, __fmul_rn(beta, D));
+    g = __fadd_rn(g, __fmul_rn(__fsub_rn(z, zb), inv_beta));
     return g;
 }
 __device__ __forceinline__ float clamp_lohi(float t, float lo, float hi) {
@@ -171,23 +179,26 @@ __device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParam
 
 // slack of row i (column j): a = sigma_i e_i, cost 0, bounds [0, inf); the new
 // value from the row's residual rv
+template <bool kFast>
 __device__ __forceinline__ float slack_new(const DevLP& L, const StepParams& P, int64_t i, int64_t j, float sig,
                                            float rv, float z) {
     float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
     float ua = 0.0f;
     if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[i] : L.ubar[i]);
-    float g = grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
+    float g = kFast ? grad_fast(0.0f, ua, D, z, zbar_of(L, j), P.beta, P.inv_beta)
+                    : grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
     float t = __fsub_rn(z, __fmul_rn(g, unit_invL(P, 1.0)));
     return t < 0.0f ? 0.0f : t;
 }
 // one slack step with a plain read-modify-write of r (rows of distinct slacks differ)
+template <bool kFast>
 __device__ __forceinline__ void update_slack(const DevLP& L, const StepParams& P, int64_t q) {
     const int64_t i = slack_row_of(L, q);
     const int64_t j = L.n_s + q;
     const float sig = row_sigma(L, i);
     const float rv = L.r[i];
     const float z = L.z[j];
-    const float zn = slack_new(L, P, i, j, sig, rv, z);
+    const float zn = slack_new<kFast>(L, P, i, j, sig, rv, z);
     const float d = __fsub_rn(zn, z);
     if (d != 0.0f) L.r[i] = __fadd_rn(rv, sig < 0.0f ? -d : d);
     L.z[j] = zn;
@@ -254,7 +265,7 @@ __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const 
 
 __global__ void __launch_bounds__(256) k_det_slacks(DevLP L, StepParams P) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L.n_ineq; q += (int64_t)gridDim.x * blockDim.x)
-        update_slack(L, P, q);
+        update_slack<false>(L, P, q);
 }
 
 // ------------------------------------------------------------ async
@@ -284,7 +295,7 @@ __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P
     for (int l = 0; l < k; l++) {
         int64_t j = f + l;
         float D = col_dot_seq<true>(L, j);
-        float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
+        float g = grad_fast(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta, P.inv_beta);
         y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
     }
     project_simplex(y, k, x);
@@ -422,7 +433,7 @@ __device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P
     if (lane >= tc.ncols || (L.unit_fixed && L.unit_fixed[tc.u0 + tc.a + lane])) return 0.0f;
     const int64_t j = tc.j0 + lane;
     float z = L.z[j];
-    float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
+    float g = grad_fast(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta, P.inv_beta);
     float invL = unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
@@ -518,7 +529,7 @@ __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
     const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
     if (j >= L.n_scalar) return;
     float z = L.z[j];
-    float g = grad_from(c_int(L, j), ua_of(L, j), H.buf[i], z, zbar_of(L, j), P.beta);
+    float g = grad_fast(c_int(L, j), ua_of(L, j), H.buf[i], z, zbar_of(L, j), P.beta, P.inv_beta);
     float invL = unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
@@ -530,31 +541,34 @@ __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
 __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H, float* acc_next) {
     const int lane = threadIdx.x & 31;
     const int64_t span = (int64_t)gridDim.x * blockDim.x;
-    const bool lmax = P.rule == THETIS_STEP_LMAX;
     for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
          e0 += kRowsPerThread * span) {
         int2 sl[kRowsPerThread];
+        bool take[kRowsPerThread];
         float r0[kRowsPerThread], z[kRowsPerThread];
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
             const int64_t e = e0 + q * span;
-            const bool ok = e < L.m;
-            sl[q] = ok ? H.row_slot[e] : make_int2(-1, -1);
-            r0[q] = ok ? L.r[e] : 0.0f;
-            z[q] = ok ? L.z[L.n_s + e] : 0.0f;
+            sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
+            take[q] = e < L.m;
+            r0[q] = take[q] ? L.r[e] : 0.0f;
+            z[q] = take[q] ? L.z[L.n_s + e] : 0.0f;
         }
-        float rv[kRowsPerThread];
+        float rv[kRowsPerThread], du[kRowsPerThread], dv[kRowsPerThread];
+#pragma unroll
+        for (int q = 0; q < kRowsPerThread; q++) { // all hub-step loads in flight together
+            du[q] = take[q] && sl[q].x >= 0 ? H.buf[sl[q].x] : 0.0f;
+            dv[q] = take[q] && sl[q].y >= 0 ? H.buf[sl[q].y] : 0.0f;
+        }
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
             const int64_t e = e0 + q * span;
-            float delta = 0.0f;
-            if (sl[q].x >= 0) delta = H.buf[sl[q].x];
-            if (sl[q].y >= 0) delta = __fadd_rn(delta, H.buf[sl[q].y]);
+            const float delta = __fadd_rn(du[q], dv[q]);
             rv[q] = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
-            if (e < L.m) {
+            if (take[q]) {
                 const int64_t j = L.n_s + e;
                 const float sig = row_sigma(L, e);
-                const float zn = slack_new(L, P, e, j, sig, rv[q], z[q]);
+                const float zn = slack_new<true>(L, P, e, j, sig, rv[q], z[q]);
                 const float d = __fsub_rn(zn, z[q]);
                 if (d != 0.0f) {
                     rv[q] = __fadd_rn(rv[q], sig < 0.0f ? -d : d);
@@ -563,12 +577,11 @@ __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, H
                 if (rv[q] != r0[q]) L.r[e] = rv[q];
             }
         }
-        (void)lmax;
         // a hub-hub row is not touched again before the next epoch's hub step:
         // add its final r_e to the next epoch's accumulators now
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
-            const bool hh = sl[q].x >= 0 && sl[q].y >= 0;
+            const bool hh = take[q] && sl[q].x >= 0 && sl[q].y >= 0;
             if (hh) atomicAdd(acc_next + sl[q].x, rv[q]);
             add_max_side(acc_next, hh ? sl[q].y : -1, rv[q], lane);
         }
@@ -577,7 +590,7 @@ __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, H
 // (2) without a hub step: the slack sweep
 __global__ void __launch_bounds__(256) k_slack_sweep(DevLP L, StepParams P) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < L.n_ineq; q += (int64_t)gridDim.x * blockDim.x)
-        update_slack(L, P, q);
+        update_slack<true>(L, P, q);
 }
 
 struct AsyncCtx {
@@ -753,6 +766,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     StepParams P{};
     P.beta = beta;
     P.beta_d = (double)beta;
+    P.inv_beta = (float)(1.0 / (double)beta);
     P.rule = step_rule;
     const double Lmax = (double)beta * lp->maxnorm2 + 1.0 / (double)beta; // Eq. 7
     P.invLmax = (float)(1.0 / Lmax);

@@ -166,7 +166,7 @@ struct Carver {
 struct thetis_lp {
     thetis::DevLP d{};
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;   // concurrent stream for heavy async tiles
+    cudaStream_t side = nullptr;   // second stream: hub-hub row pass beside the light tiles
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_epoch;
     char* ws = nullptr;
