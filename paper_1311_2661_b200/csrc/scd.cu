@@ -391,8 +391,10 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
     __syncwarp();
 }
 // r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]
+// hub_next / row_slot (VC / MIS with a hub step): a step scattered to a row whose
+// other endpoint is a hub is also added to that hub's next-epoch accumulator
 __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                              int lane) {
+                                              int lane, float* hub_next = nullptr, const int2* row_slot = nullptr) {
     constexpr int U = 4;
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
@@ -421,7 +423,14 @@ __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int 
             }
             if (t < c1 && d != 0.0f) {
                 const float a = L.val ? L.val[t] : ((raw[q] & kSignBit) ? -1.0f : 1.0f);
-                red_add(L.r + (raw[q] & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
+                const float ad = L.val ? a * d : (a < 0.0f ? -d : d);
+                const uint32_t row = raw[q] & kRowMask;
+                red_add(L.r + row, ad);
+                if (hub_next) {
+                    const int2 sl = row_slot[row];
+                    const int slot = sl.x > sl.y ? sl.x : sl.y; // the tile's own column is light
+                    if (slot >= 0) atomicAdd(hub_next + slot, ad);
+                }
             }
         }
     }
@@ -577,13 +586,13 @@ __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, H
                 if (rv[q] != r0[q]) L.r[e] = rv[q];
             }
         }
-        // a hub-hub row is not touched again before the next epoch's hub step:
-        // add its final r_e to the next epoch's accumulators now
+        // the next epoch's hub dot products: r_e as it leaves this pass (a hub-hub row
+        // is not touched again; a row with a light endpoint gets the light tile's step
+        // added to the accumulator by that tile, see scatter_range)
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
-            const bool hh = take[q] && sl[q].x >= 0 && sl[q].y >= 0;
-            if (hh) atomicAdd(acc_next + sl[q].x, rv[q]);
-            add_max_side(acc_next, hh ? sl[q].y : -1, rv[q], lane);
+            if (take[q] && sl[q].x >= 0) atomicAdd(acc_next + sl[q].x, rv[q]);
+            add_max_side(acc_next, take[q] ? sl[q].y : -1, rv[q], lane);
         }
     }
 }
@@ -598,6 +607,8 @@ struct AsyncCtx {
     int64_t n_tiles, heavy_limit;  // tiles above heavy_limit were done by the hub step
     unsigned long long* next;      // position counters (one per stream, 256 B apart)
     int streams;
+    float* hub_next;               // next epoch's hub accumulators (or nullptr)
+    const int2* row_slot;
 };
 
 // (3) One tile of structural units by one warp, tile-synchronous: all units
@@ -633,7 +644,7 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
             L.z[j] = xb[l];
         }
     }
-    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane);
+    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane, C.hub_next, C.row_slot);
     __syncwarp();
 }
 
@@ -830,9 +841,13 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 float* acc_next = H.buf == hub_acc[0] ? hub_acc[1] : hub_acc[0];
                 if (e == 0) CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
                 CUDA_TRY(lp, cudaMemsetAsync(acc_next, 0, (size_t)H.n_heavy * 32 * 4, s));
-                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf, e == 0 ? 0 : 1);
+                // a solve's first epoch gathers D from the rows; later epochs find it
+                // already accumulated by the previous row pass and light tiles
+                if (e == 0) k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf, 0);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
                 k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H, acc_next);
+                AC.hub_next = acc_next;
+                AC.row_slot = H.row_slot;
                 H.buf = acc_next;
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);

@@ -182,3 +182,23 @@ def test_config5_full_properties_bench_launch(th):
     assert res["cost"] <= float(w.double().sum())
     if eps < 1:
         assert res["cost"] <= 2 * o["lp_obj"] / (1 - eps) * (1 + 1e-6)
+
+
+# ---------------------------------------------------------------- config 5 recipe, reduced
+@pytest.mark.parametrize("rule", [0, 1])
+def test_config5_reduced_async_matches_reference(th, rule):
+    # R-MAT scale 18 with config 5's (a, b, c) and edge factor: hub tiles, the hub step, the
+    # fused row pass and many concurrent light tiles (the bench's code path at reduced size)
+    cfg = inputs.CONFIGS["vc_rmat_26"]
+    g = inputs.make_graph(cfg, scale=18, samples=16 << 18)
+    lp = gpu_lp(th, g, VC)
+    r64 = ref_lp(g, VC, 64)
+    lp.solve(cfg.beta, 8, mode=1, seed=cfg.solve_seed, step_rule=rule)
+    r64.solve(cfg.beta, 8, mode=oracle.MODE_TILE_SYNC, seed=cfg.solve_seed, step_rule=rule)
+    o, ro = lp.objective(cfg.beta), r64.objective(cfg.beta)
+    assert o["f_beta"] == pytest.approx(ro["f_beta"], rel=1e-3)
+    assert o["lp_obj"] == pytest.approx(ro["lp_obj"], rel=1e-3)
+    assert o["drift_inf"] < 1e-4
+    _, res = lp.round(1)
+    _, rres = r64.round(1)
+    assert res["feasible"] == 1 and res["cost"] == pytest.approx(rres["cost"], rel=1e-2)
