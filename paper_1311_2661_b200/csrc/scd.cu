@@ -391,10 +391,8 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
     __syncwarp();
 }
 // r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]
-// hub_next / row_slot (VC / MIS with a hub step): a step scattered to a row whose
-// other endpoint is a hub is also added to that hub's next-epoch accumulator
 __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                              int lane, float* hub_next = nullptr, const int2* row_slot = nullptr) {
+                                              int lane) {
     constexpr int U = 4;
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
@@ -423,14 +421,7 @@ __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int 
             }
             if (t < c1 && d != 0.0f) {
                 const float a = L.val ? L.val[t] : ((raw[q] & kSignBit) ? -1.0f : 1.0f);
-                const float ad = L.val ? a * d : (a < 0.0f ? -d : d);
-                const uint32_t row = raw[q] & kRowMask;
-                red_add(L.r + row, ad);
-                if (hub_next) {
-                    const int2 sl = row_slot[row];
-                    const int slot = sl.x > sl.y ? sl.x : sl.y; // the tile's own column is light
-                    if (slot >= 0) atomicAdd(hub_next + slot, ad);
-                }
+                red_add(L.r + (raw[q] & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
             }
         }
     }
@@ -506,10 +497,8 @@ __device__ __forceinline__ void add_max_side(float* acc, int key, float val, int
 }
 // (1a) r_e into the accumulators of the hub endpoints: the min endpoint by an
 // atomic per row, the max endpoint by add_max_side.  kRowsPerThread rows per
-// thread, all loads issued before any atomic.  With light_only, rows whose
-// endpoints are both hubs are skipped: the previous epoch's row pass already
-// added their (since unchanged) r_e.
-__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, float* acc, int light_only) {
+// thread, all loads issued before any atomic.
+__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, float* acc) {
     const int lane = threadIdx.x & 31;
     const int64_t span = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
@@ -520,7 +509,6 @@ __global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, floa
         for (int q = 0; q < kRowsPerThread; q++) {
             const int64_t e = e0 + q * span;
             sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
-            if (light_only && sl[q].x >= 0 && sl[q].y >= 0) sl[q] = make_int2(-1, -1);
             rv[q] = (sl[q].x >= 0 || sl[q].y >= 0) ? ld_cg(L.r + e) : 0.0f;
         }
 #pragma unroll
@@ -547,7 +535,7 @@ __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
 // (2) fused with the end of (1): per row, add the hub steps of both endpoints to
 // r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has
 // slack column n + e); one read-modify-write of r and s per row
-__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H, float* acc_next) {
+__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H) {
     const int lane = threadIdx.x & 31;
     const int64_t span = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
@@ -586,14 +574,6 @@ __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, H
                 if (rv[q] != r0[q]) L.r[e] = rv[q];
             }
         }
-        // the next epoch's hub dot products: r_e as it leaves this pass (a hub-hub row
-        // is not touched again; a row with a light endpoint gets the light tile's step
-        // added to the accumulator by that tile, see scatter_range)
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) {
-            if (take[q] && sl[q].x >= 0) atomicAdd(acc_next + sl[q].x, rv[q]);
-            add_max_side(acc_next, take[q] ? sl[q].y : -1, rv[q], lane);
-        }
     }
 }
 // (2) without a hub step: the slack sweep
@@ -607,8 +587,6 @@ struct AsyncCtx {
     int64_t n_tiles, heavy_limit;  // tiles above heavy_limit were done by the hub step
     unsigned long long* next;      // position counters (one per stream, 256 B apart)
     int streams;
-    float* hub_next;               // next epoch's hub accumulators (or nullptr)
-    const int2* row_slot;
 };
 
 // (3) One tile of structural units by one warp, tile-synchronous: all units
@@ -644,7 +622,7 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
             L.z[j] = xb[l];
         }
     }
-    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane, C.hub_next, C.row_slot);
+    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane);
     __syncwarp();
 }
 
@@ -787,7 +765,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     AsyncCtx AC{};
     HubCtx H{};
     int64_t blocks = 1, hub_blocks = 1, workers = 1;
-    float* hub_acc[2] = {nullptr, nullptr};
     int batch = 1;
     if (mode != THETIS_MODE_DETERMINISTIC) {
         THETIS_TRY(ensure_heavy(lp));
@@ -803,9 +780,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         int32_t* hub_id = C.take<int32_t>(n_tiles);
         H.row_slot = row_slot;
         H.hub_id = hub_id;
-        hub_acc[0] = C.take<float>(H.n_heavy * 32);
-        hub_acc[1] = C.take<float>(H.n_heavy * 32);
-        H.buf = hub_acc[0];
+        H.buf = C.take<float>(H.n_heavy * 32);
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
         if (H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
@@ -835,20 +810,11 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         } else {
             // (1) hub step + (2) slack sweep, fused; or (2) alone
             if (H.n_heavy > 0) {
-                // accumulators ping-pong: the hub-hub part of this epoch's D was added
-                // by the previous epoch's row pass (except in a solve's first epoch)
                 const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
-                float* acc_next = H.buf == hub_acc[0] ? hub_acc[1] : hub_acc[0];
-                if (e == 0) CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
-                CUDA_TRY(lp, cudaMemsetAsync(acc_next, 0, (size_t)H.n_heavy * 32 * 4, s));
-                // a solve's first epoch gathers D from the rows; later epochs find it
-                // already accumulated by the previous row pass and light tiles
-                if (e == 0) k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf, 0);
+                CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
+                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
-                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H, acc_next);
-                AC.hub_next = acc_next;
-                AC.row_slot = H.row_slot;
-                H.buf = acc_next;
+                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H);
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
             }
