@@ -471,7 +471,7 @@ __global__ void k_row_slots(DevLP L, HubCtx H, int2* row_slot) {
     }
 }
 
-constexpr int kRowsPerThread = 4;
+constexpr int kRowsPerThread = 8;
 
 // v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
 // not a hub); add the warp's run segments with one atomic each.  Fast path when
