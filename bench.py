@@ -53,6 +53,23 @@ def parse():
     return p.parse_args()
 
 
+def max_over_ranks(x: float, device=None) -> float:
+    """max of a host scalar over all ranks (NCCL on the GPU, gloo on the CPU); the value
+    itself when not distributed"""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(units_per_step_per_rank: float, steps: int, world: int, ms_max: float) -> float:
+    """whole-job throughput: the units all ranks processed over the max-over-ranks time"""
+    return units_per_step_per_rank * steps * world / (ms_max / 1e3)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -216,18 +233,13 @@ def run_thetis(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     clocks = clk.summary()
-    if ws_n > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     last = recs[-1]
     dims = last["dims"]
     upd_step = last["st"].coordinate_updates
     nnz_step = last["st"].nnz_processed
-    value = upd_step * args.steps * ws_n / (ms / 1e3)
+    value = job_throughput(upd_step, args.steps, ws_n, ms)
     ep_med = statistics.median(epoch_ms)
     b_epoch = algorithmic_bytes(dims.n_struct, dims.nnz_struct, dims.m)
     peak, peak_src = load_peaks()
@@ -255,13 +267,8 @@ def run_thetis(args):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms_e2e = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
-        if ws_n > 1:
-            import torch.distributed as dist
-            t = torch.tensor([ms_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": upd_step * ke * ws_n / (ms_e2e / 1e3), "unit": "coordinate updates/s",
+        ms_e2e = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3), dev)
+        e2e = {"value": job_throughput(upd_step, ke, ws_n, ms_e2e), "unit": "coordinate updates/s",
                "h2d_bytes_per_step": 8 * E + 4 * n, "d2h_bytes_per_step": n + ctypes.sizeof(th.RoundResult),
                "ms_per_step": ms_e2e / ke}
 
@@ -271,6 +278,10 @@ def run_thetis(args):
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and ws_n == 1:
         cpu = cpu_baseline()
+    if ws_n > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
         return
     ob, rr = last["ob"], last["rr"]
