@@ -447,14 +447,27 @@ __device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P
 // adds r_e into the (L2-resident) accumulators of the hub endpoints, the update
 // takes the hub steps, the scatter adds the hub steps of both endpoints to r_e
 // with a plain read-modify-write (the hub phase runs alone).
+// The hottest hubs (top kMaxHot by degree) receive ~1e6 min-side additions per epoch;
+// same-address atomics serialise at their L2 slice, so each of them gets kReplicas
+// accumulator copies (spread by warp), folded before the update.
+constexpr int kMaxHot = 8192;
+constexpr int kReplicas = 32;
+constexpr int32_t kHotBit = 1 << 30;  // in row_slot.x: the value is a hot id, not a slot
 struct HubCtx {
     int64_t n_heavy;
     const int32_t* heavy_tiles;  // sorted tile ids
     const int32_t* hub_id;       // per structural tile: index in heavy_tiles, or -1
-    const int2* row_slot;        // per row: accumulator slots of (min, max) endpoint, -1 if not a hub
+    const int2* row_slot;        // per row: accumulator slots of (min, max) endpoint, -1 if not a hub;
+                                 // .x = kHotBit | hot id for a hot min endpoint
     float* buf;                  // compact accumulators, transposed: [lane][hub id] (L2-resident,
                                  // and the top hubs 0, 1, 2, 4, ... fall in different lines)
+    const int32_t* hot_slot;     // hot id -> slot
+    float* hotbuf;               // [hot id][kReplicas]
+    int64_t n_hot;
 };
+__device__ __forceinline__ int32_t plain_slot(const HubCtx& H, int32_t x) {
+    return (x >= 0 && (x & kHotBit)) ? H.hot_slot[x & ~kHotBit] : x;
+}
 __device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int64_t v) {
     const int32_t h = H.hub_id[v >> 5];
     return h < 0 ? -1 : (int32_t)((v & 31) * H.n_heavy + h);
@@ -464,11 +477,45 @@ __global__ void k_hub_ids(int64_t n_heavy, const int32_t* heavy_tiles, int32_t* 
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n_heavy; h += (int64_t)gridDim.x * blockDim.x)
         hub_id[heavy_tiles[h]] = (int32_t)h;
 }
-__global__ void k_row_slots(DevLP L, HubCtx H, int2* row_slot) {
+__global__ void k_row_slots(DevLP L, HubCtx H, const int32_t* hot_of_slot, int2* row_slot) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
         const int2 uv = L.edges[e];
-        row_slot[e] = make_int2(hub_slot(H, uv.x), hub_slot(H, uv.y));
+        int32_t x = hub_slot(H, uv.x);
+        if (x >= 0 && hot_of_slot[x] >= 0) x = kHotBit | hot_of_slot[x];
+        row_slot[e] = make_int2(x, hub_slot(H, uv.y));
     }
+}
+// log2-degree histogram of the hub columns, to pick the hot threshold
+__global__ void k_hub_deg_hist(DevLP L, HubCtx H, unsigned long long* hist) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H.n_heavy * 32; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
+        if (j >= L.n_scalar) continue;
+        const int64_t d = L.colptr[j + 1] - L.colptr[j];
+        atomicAdd(hist + (d > 0 ? 63 - __clzll(d) : 0), 1ull);
+    }
+}
+__global__ void k_hot_assign(DevLP L, HubCtx H, int64_t thr, int64_t hot_cap, int32_t* hot_of_slot,
+                             int32_t* hot_slot, unsigned long long* count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H.n_heavy * 32; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = i >> 5, lane = i & 31;
+        const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
+        const int32_t slot = (int32_t)(lane * H.n_heavy + h);
+        hot_of_slot[slot] = -1;
+        if (j >= L.n_scalar || L.colptr[j + 1] - L.colptr[j] < thr) continue;
+        const unsigned long long id = atomicAdd(count, 1ull);
+        if (id < (unsigned long long)hot_cap) {
+            hot_of_slot[slot] = (int32_t)id;
+            hot_slot[id] = slot;
+        }
+    }
+}
+// hot replicas -> the plain accumulators (after the gather, before the update)
+__global__ void k_hot_fold(HubCtx H) {
+    const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (h >= H.n_hot) return;
+    float s = 0.0f;
+    for (int q = 0; q < kReplicas; q++) s += H.hotbuf[h * kReplicas + q];
+    H.buf[H.hot_slot[h]] += s;
 }
 
 constexpr int kRowsPerThread = 8;
@@ -513,7 +560,12 @@ __global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, floa
         }
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) {
-            if (sl[q].x >= 0) atomicAdd(acc + sl[q].x, rv[q]);
+            if (sl[q].x >= 0) {
+                if (sl[q].x & kHotBit)
+                    atomicAdd(H.hotbuf + (int64_t)(sl[q].x & ~kHotBit) * kReplicas + ((threadIdx.x >> 5) + blockIdx.x) % kReplicas, rv[q]);
+                else
+                    atomicAdd(acc + sl[q].x, rv[q]);
+            }
             add_max_side(acc, sl[q].y, rv[q], lane);
         }
     }
@@ -554,7 +606,7 @@ __global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, H
         float rv[kRowsPerThread], du[kRowsPerThread], dv[kRowsPerThread];
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; q++) { // all hub-step loads in flight together
-            du[q] = take[q] && sl[q].x >= 0 ? H.buf[sl[q].x] : 0.0f;
+            du[q] = take[q] && sl[q].x >= 0 ? H.buf[plain_slot(H, sl[q].x)] : 0.0f;
             dv[q] = take[q] && sl[q].y >= 0 ? H.buf[sl[q].y] : 0.0f;
         }
 #pragma unroll
@@ -781,11 +833,34 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         H.row_slot = row_slot;
         H.hub_id = hub_id;
         H.buf = C.take<float>(H.n_heavy * 32);
+        // hot replicas only when there are hubs (the buffer doubles as the degree histogram)
+        const int64_t hot_cap = H.n_heavy * 32 < kMaxHot ? H.n_heavy * 32 : kMaxHot;
+        int32_t* hot_of_slot = C.take<int32_t>(H.n_heavy * 32);
+        int32_t* hot_slot = C.take<int32_t>(hot_cap);
+        H.hot_slot = hot_slot;
+        H.hotbuf = C.take<float>(H.n_heavy > 0 ? (hot_cap * kReplicas > 160 ? hot_cap * kReplicas : 160) : 1);
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
         if (H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
             k_hub_ids<<<grid_for(H.n_heavy, 256), 256, 0, s>>>(H.n_heavy, H.heavy_tiles, hub_id);
-            k_row_slots<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, row_slot);
+            // hot hubs: the smallest power-of-two degree threshold with <= kMaxHot above it
+            std::vector<unsigned long long> hh(64, 0);
+            unsigned long long* dhist = (unsigned long long*)H.hotbuf; // scratch before use
+            CUDA_TRY(lp, cudaMemsetAsync(dhist, 0, 64 * 8 + 8, s));
+            k_hub_deg_hist<<<grid_for(H.n_heavy * 32, 256), 256, 0, s>>>(L, H, dhist);
+            CUDA_TRY(lp, cudaMemcpyAsync(hh.data(), dhist, 64 * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+            int b = 63;
+            unsigned long long above = 0;
+            while (b > 0 && above + hh[b] <= (unsigned long long)hot_cap) above += hh[b--];
+            const int64_t thr = (int64_t)1 << (b + 1);
+            CUDA_TRY(lp, cudaMemsetAsync(dhist, 0, 8, s));
+            k_hot_assign<<<grid_for(H.n_heavy * 32, 256), 256, 0, s>>>(L, H, thr, hot_cap, hot_of_slot, hot_slot, dhist);
+            unsigned long long nh = 0;
+            CUDA_TRY(lp, cudaMemcpyAsync(&nh, dhist, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+            H.n_hot = nh < (unsigned long long)hot_cap ? (int64_t)nh : hot_cap;
+            k_row_slots<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, hot_of_slot, row_slot);
         }
         AC.n_tiles = n_tiles;
         AC.heavy_limit = hub_step_enabled(L) ? kHeavy : INT64_MAX;
@@ -812,7 +887,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (H.n_heavy > 0) {
                 const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
                 CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
+                if (H.n_hot > 0) CUDA_TRY(lp, cudaMemsetAsync(H.hotbuf, 0, (size_t)H.n_hot * kReplicas * 4, s));
                 k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf);
+                if (H.n_hot > 0) k_hot_fold<<<(unsigned)((H.n_hot + 255) / 256), 256, 0, s>>>(H);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
                 k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H);
             } else if (L.n_ineq > 0) {
