@@ -19,7 +19,7 @@
 #endif
 
 #define GOLDEN 0x9E3779B97F4A7C15ULL
-#define HUB_NNZ 2048 /* R-6: tiles whose scalar columns hold more nonzeros are hub tiles */
+#define HUB_NNZ 512 /* R-6: tiles whose scalar columns hold more nonzeros are hub tiles */
 
 enum { PROB_GENERIC = 0, PROB_VC = 1, PROB_MIS = 2, PROB_MWC = 3 };
 enum { SENSE_EQ = 0, SENSE_GE = 1, SENSE_LE = 2 };

@@ -98,7 +98,7 @@ double thetis_ref_grad(const ref_lp* lp, float beta, int64_t j);
  * mode 2 = plain cyclic sweep;
  * mode 3 = the async reference trajectory (R-6), per epoch: (1) VC / MIS:
  *          the scalar columns of the hub tiles (tiles of 32 structural units
- *          whose columns hold > 2048 nonzeros) take one synchronous step;
+ *          whose columns hold > 512 nonzeros) take one synchronous step;
  *          (2) every slack takes its step (slacks share no row); (3) the tiles
  *          of 32 structural units in permutation order (pi_e over the
  *          structural tiles), each one synchronous step of its units (every

@@ -33,7 +33,7 @@ namespace thetis {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int64_t kHeavy = 2048;    // async: scalar nnz per tile above which the tile is split
+constexpr int64_t kHeavy = 512;     // async: a tile whose scalar columns hold more nonzeros is a hub tile (R-6)
 constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the warp path
 
 struct StepParams {
