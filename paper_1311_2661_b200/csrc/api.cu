@@ -226,30 +226,8 @@ THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uin
     if (lp->anchors) THETIS_TRY(recompute_ua(lp));
     THETIS_TRY(solve_epochs(lp, beta, epochs, mode, seed, step_rule, stats));
     if (stats) {
-        // per-epoch work: every non-fixed unit once
-        int64_t upd = 0, nnz = 0;
-        const DevLP& d = lp->d;
-        upd = lp->d.n_ineq;
-        nnz = lp->d.n_ineq;
-        // structural counts are exact for graph LPs without fixed units; with
-        // fixed units (MWC terminals, generic lo == hi) they are computed below
-        std::vector<uint8_t> fixed;
-        const int64_t S = d.n_blocks + d.n_scalar;
-        if (d.unit_fixed && S > 0) {
-            fixed.resize(S);
-            CUDA_TRY(lp, cudaMemcpy(fixed.data(), d.unit_fixed, (size_t)S, cudaMemcpyDeviceToHost));
-        }
-        std::vector<int64_t> cp(d.n_s + 1);
-        if (d.n_s >= 0) CUDA_TRY(lp, cudaMemcpy(cp.data(), d.colptr, (size_t)(d.n_s + 1) * 8, cudaMemcpyDeviceToHost));
-        for (int64_t u = 0; u < S; u++) {
-            if (!fixed.empty() && fixed[u]) continue;
-            int64_t f = u < d.n_blocks ? u * d.k : d.n_blocks * d.k + (u - d.n_blocks);
-            int64_t c = u < d.n_blocks ? d.k : 1;
-            upd += c;
-            nnz += cp[f + c] - cp[f];
-        }
-        stats->coordinate_updates = upd * epochs;
-        stats->nnz_processed = nnz * epochs;
+        stats->coordinate_updates = lp->epoch_updates * epochs;
+        stats->nnz_processed = lp->epoch_nnz * epochs;
     }
     return THETIS_OK;
 }

@@ -318,6 +318,27 @@ __global__ void k_recompute_ua(DevLP L) {
     }
 }
 
+// per-epoch work: every non-fixed unit once (coordinates, nonzeros incl. slacks)
+__global__ void k_epoch_work(DevLP L, unsigned long long* out) {
+    unsigned long long upd = 0, nnz = 0;
+    const int64_t S = L.n_blocks + L.n_scalar;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
+        if (L.unit_fixed && L.unit_fixed[u]) continue;
+        const int64_t f = u < L.n_blocks ? u * L.k : L.n_blocks * L.k + (u - L.n_blocks);
+        const int64_t c = u < L.n_blocks ? L.k : 1;
+        upd += (unsigned long long)c;
+        nnz += (unsigned long long)(L.colptr[f + c] - L.colptr[f]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (upd || nnz)) {
+        atomicAdd(out, upd);
+        atomicAdd(out + 1, nnz);
+    }
+}
+
 int bits_for(uint64_t v) {
     int b = 0;
     while (b < 64 && (v >> b) != 0) b++;
@@ -547,6 +568,20 @@ static void fill_units(thetis_lp* lp) {
     d.U = d.n_blocks + d.n_scalar + d.n_ineq;
 }
 
+// the work of one epoch (stats), counted once per LP after the bounds are known
+static int count_epoch_work(thetis_lp* lp) {
+    unsigned long long* w = (unsigned long long*)(lp->flags + 24);
+    CUDA_TRY(lp, cudaMemsetAsync(w, 0, 16, lp->stream));
+    const int64_t S = lp->d.n_blocks + lp->d.n_scalar;
+    if (S > 0) k_epoch_work<<<grid_for(S, T), T, 0, lp->stream>>>(lp->d, w);
+    unsigned long long h[2] = {0, 0};
+    CUDA_TRY(lp, cudaMemcpyAsync(h, w, 16, cudaMemcpyDeviceToHost, lp->stream));
+    CUDA_TRY(lp, cudaStreamSynchronize(lp->stream));
+    lp->epoch_updates = (int64_t)h[0] + lp->d.n_ineq;
+    lp->epoch_nnz = (int64_t)h[1] + lp->d.n_ineq;
+    return THETIS_OK;
+}
+
 int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t* src, const int32_t* dst,
                 const float* vertex_w, const float* edge_w, int k, const int32_t* terminals, int t_per_label) {
     GraphTemps t{};
@@ -688,7 +723,7 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     if (h[FLAG_DUP_TERMINAL]) return set_error(lp, THETIS_ERR_INVALID_ARG, "a vertex is a terminal twice");
     lp->maxnorm2 = (double)md;
     if (d.n_ineq > 0 && lp->maxnorm2 < 1.0) lp->maxnorm2 = 1.0; // slack columns
-    return THETIS_OK;
+    return count_epoch_work(lp);
 }
 
 int build_generic(thetis_lp* lp, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
@@ -773,7 +808,7 @@ int build_generic(thetis_lp* lp, int64_t m, int64_t n, int64_t nnz, const int64_
     memcpy(&mxd, &hfp[2], 8);
     lp->maxnorm2 = mxd;
     if (d.n_ineq > 0 && lp->maxnorm2 < 1.0) lp->maxnorm2 = 1.0;
-    return THETIS_OK;
+    return count_epoch_work(lp);
 }
 
 }  // namespace thetis

@@ -43,8 +43,20 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(DevLP L, double beta, do
         q[Q_PROX] += d * d;
         if (!isfinite(z)) q[Q_NONFIN] = 1.0;
     }
-    for (int64_t i = tid; i < L.m; i += stride) {
-        double ax = row_ax(L, i);
+    // rows four at a time: the edge and z gathers of four rows are in flight together
+    constexpr int kU = 4;
+    for (int64_t i0 = tid; i0 < L.m; i0 += kU * stride) {
+        double axs[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const int64_t i = i0 + u * stride;
+            axs[u] = i < L.m ? row_ax(L, i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+        const int64_t i = i0 + u * stride;
+        if (i >= L.m) break;
+        const double ax = axs[u];
         int64_t sl = row_slack_of(L, i);
         double sv = sl >= 0 ? (double)row_sigma(L, i) * (double)L.z[sl] : 0.0;
         double b = (double)row_b(L, i);
@@ -58,6 +70,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(DevLP L, double beta, do
         int s = row_sense(L, i);
         double viol = s == THETIS_GE ? b - ax : (s == THETIS_LE ? ax - b : fabs(ax - b));
         q[Q_EPS] = fmax(q[Q_EPS], viol);
+        }
     }
     __shared__ double sh[Q_ALL][kRedThreads];
     for (int i = 0; i < Q_ALL; i++) sh[i][threadIdx.x] = q[i];

@@ -26,14 +26,28 @@ struct CkrParams {
 __device__ __forceinline__ void atomic_max_nonneg(float* p, float v) {
     if (v > 0.0f) atomicMax((int*)p, __float_as_int(v));
 }
+// max over the block (non-negative floats compare like their bit patterns), one
+// atomic per block
+__device__ __forceinline__ void block_max_nonneg(float* p, float v) {
+    __shared__ float sh[32];
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0f;
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) atomic_max_nonneg(p, v);
+    }
+}
 
 // ---------------- VC
 __global__ void k_vc_eps(int64_t m, const int2* __restrict__ edges, const float* __restrict__ x, float* eps) {
+    float best = 0.0f;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         int2 uv = edges[e];
-        float v = __fsub_rn(1.0f, __fadd_rn(x[uv.x], x[uv.y]));
-        atomic_max_nonneg(eps, v);
+        best = fmaxf(best, __fsub_rn(1.0f, __fadd_rn(x[uv.x], x[uv.y])));
     }
+    block_max_nonneg(eps, best);
 }
 __global__ void k_vc_select(int64_t n, int rule, const float* __restrict__ x, const float* eps_p, uint8_t* sel,
                             uint8_t* add, int32_t* fallback) {
@@ -102,11 +116,12 @@ __global__ void k_sum_partials(int blocks, int width, const double* partial, dou
 
 // ---------------- MIS
 __global__ void k_mis_alpha(int64_t m, const int2* __restrict__ edges, const float* __restrict__ x, float* alpha) {
+    float best = 0.0f;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         int2 uv = edges[e];
-        float v = __fsub_rn(__fadd_rn(x[uv.x], x[uv.y]), 1.0f);
-        atomic_max_nonneg(alpha, v);
+        best = fmaxf(best, __fsub_rn(__fadd_rn(x[uv.x], x[uv.y]), 1.0f));
     }
+    block_max_nonneg(alpha, best);
 }
 // w precedes v in (x desc, w desc, id asc)
 __device__ __forceinline__ bool mis_precedes(float xw, float ww, int64_t w, float xv, float wv, int64_t v) {

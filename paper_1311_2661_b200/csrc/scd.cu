@@ -487,12 +487,17 @@ __global__ void k_row_slots(DevLP L, HubCtx H, const int32_t* hot_of_slot, int2*
 }
 // log2-degree histogram of the hub columns, to pick the hot threshold
 __global__ void k_hub_deg_hist(DevLP L, HubCtx H, unsigned long long* hist) {
+    __shared__ unsigned long long sh[64];
+    if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+    __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H.n_heavy * 32; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
         if (j >= L.n_scalar) continue;
         const int64_t d = L.colptr[j + 1] - L.colptr[j];
-        atomicAdd(hist + (d > 0 ? 63 - __clzll(d) : 0), 1ull);
+        atomicAdd(sh + (d > 0 ? 63 - __clzll(d) : 0), 1ull);
     }
+    __syncthreads();
+    if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
 }
 __global__ void k_hot_assign(DevLP L, HubCtx H, int64_t thr, int64_t hot_cap, int32_t* hot_of_slot,
                              int32_t* hot_slot, unsigned long long* count) {
@@ -574,15 +579,16 @@ __global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, floa
 __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= H.n_heavy * 32) return;
-    const int64_t h = i % H.n_heavy, lane = i / H.n_heavy; // slot i = lane * n_heavy + h
+    const int64_t h = i >> 5, lane = i & 31;  // consecutive threads: consecutive columns
     const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
     if (j >= L.n_scalar) return;
+    const int64_t slot = lane * H.n_heavy + h;
     float z = L.z[j];
-    float g = grad_fast(c_int(L, j), ua_of(L, j), H.buf[i], z, zbar_of(L, j), P.beta, P.inv_beta);
-    float invL = unit_invL(P, col_norm2(L, j));
+    float g = grad_fast(c_int(L, j), ua_of(L, j), H.buf[slot], z, zbar_of(L, j), P.beta, P.inv_beta);
+    float invL = P.rule == THETIS_STEP_LMAX ? P.invLmax : unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
-    H.buf[i] = __fsub_rn(zn, z);
+    H.buf[slot] = __fsub_rn(zn, z);
 }
 // (2) fused with the end of (1): per row, add the hub steps of both endpoints to
 // r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has

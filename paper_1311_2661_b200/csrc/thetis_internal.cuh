@@ -180,6 +180,8 @@ struct thetis_lp {
     int32_t* members = nullptr;    // class members, grouped by class
     int32_t* heavy = nullptr;      // heavy async tiles
     double maxnorm2 = 0;           // max_j ||a_j||^2 over all standard-form columns
+    int64_t epoch_updates = 0;     // coordinates updated per epoch (stats)
+    int64_t epoch_nnz = 0;         // nonzeros processed per epoch (slack = 1)
     // colouring cache
     bool colour_valid = false;
     uint64_t colour_seed = 0;
