@@ -300,10 +300,15 @@ int thetis_ref_build_lp(ref_lp** out, int64_t m, int64_t n, int64_t nnz, const i
 /* ------------------------------------------------------------------ */
 /* graph LPs: VC (Eq. 2), MIS (App. B.2 edge rows), MWC (App. B.3)     */
 /* ------------------------------------------------------------------ */
-typedef struct { uint64_t key; int64_t idx; } keyed_edge;
+/* rows of graph LPs (R-17): (u < v) pairs sorted by
+ * (floor(u / 2^ROW_RANGE_SHIFT), v, u) */
+#define ROW_RANGE_SHIFT 14
+typedef struct { uint64_t key; int64_t idx; } keyed_edge; /* key = (v << 32) | u */
 static int cmp_keyed(const void* a, const void* b) {
     const keyed_edge* x = (const keyed_edge*)a;
     const keyed_edge* y = (const keyed_edge*)b;
+    uint64_t gx = (x->key & 0xFFFFFFFFu) >> ROW_RANGE_SHIFT, gy = (y->key & 0xFFFFFFFFu) >> ROW_RANGE_SHIFT;
+    if (gx != gy) return gx < gy ? -1 : 1;
     if (x->key != y->key) return x->key < y->key ? -1 : 1;
     return x->idx < y->idx ? -1 : (x->idx > y->idx);
 }
@@ -321,8 +326,8 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     for (int64_t e = 0; e < n_edges; e++)
         if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) return REF_INVALID_ARG;
 
-    /* canonicalise (u < v), drop self-loops, sort by (v, u), keep the first
-     * occurrence of each pair: the row order (R-17) */
+    /* canonicalise (u < v), drop self-loops, sort by (u >> 14, v, u), keep the
+     * first occurrence of each pair: the row order (R-17) */
     keyed_edge* ke = (keyed_edge*)xcalloc(n_edges, sizeof(keyed_edge));
     int64_t cnt = 0;
     for (int64_t e = 0; e < n_edges; e++) {
@@ -780,14 +785,14 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
     int64_t n_tiles = (lp->U + 31) / 32;
     const int64_t n_struct_units = lp->n_blocks + lp->n_scalar;
     const int64_t n_struct_tiles = (n_struct_units + 31) / 32;
-    int64_t* perm = (mode == MODE_ASYNC || mode == 3) ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
+    int64_t* perm = (mode == MODE_ASYNC || mode >= 3) ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
     /* hub tiles of the async reference (R-6): VC / MIS tiles whose scalar
      * columns hold more than HUB_NNZ nonzeros */
     uint8_t* hub_tile = NULL;
     int64_t* hub_cols = NULL;
     REAL* hub_new = NULL;
     int64_t n_hub_cols = 0;
-    if (mode == 3 && (lp->problem == PROB_VC || lp->problem == PROB_MIS)) {
+    if (mode >= 3 && (lp->problem == PROB_VC || lp->problem == PROB_MIS)) {
         hub_tile = (uint8_t*)xcalloc(n_struct_tiles, 1);
         hub_cols = (int64_t*)xcalloc(n_struct_tiles * 32, sizeof(int64_t));
         for (int64_t t = 0; t < n_struct_tiles; t++) {
@@ -820,34 +825,45 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                 }
         } else if (mode == 3) {
             REAL nv[32 * 64];
-            /* (1) hub step (VC / MIS): the scalar columns of every hub tile take one
-             * synchronous step from the epoch's starting state */
-            if (hub_cols) {
-                for (int64_t q = 0; q < n_hub_cols; q++) {
-                    REAL v[1];
-                    unit_new_values(lp, &s, hub_cols[q], v);
-                    hub_new[q] = v[0];
-                }
-                for (int64_t q = 0; q < n_hub_cols; q++) {
-                    int64_t u = hub_cols[q];
-                    if (unit_fixed(lp, u)) continue;
-                    nnz += apply_unit(lp, u, &hub_new[q]);
-                    updates += 1;
-                }
-            }
-            /* (2) slack sweep: slacks share no row, so any order gives the same result */
+            /* (1) the row pass: the pending hub steps of the previous epoch enter r
+             * (none in the first), then every slack takes its step (slacks share no
+             * row, so any order gives the same result) */
+            if (hub_cols && e > 0)
+                for (int64_t q = 0; q < n_hub_cols; q++) col_axpy(lp, hub_cols[q], hub_new[q]);
             for (int64_t u = n_struct_units; u < lp->U; u++) {
                 nnz += step_unit(lp, &s, u);
                 updates += 1;
             }
+            /* (2) hub step (VC / MIS): the scalar columns of every hub tile take one
+             * synchronous step from this state; z_j moves, d_j stays pending (r does
+             * not see it until the next row pass) */
+            if (hub_cols) {
+                for (int64_t q = 0; q < n_hub_cols; q++) {
+                    REAL v[1];
+                    unit_new_values(lp, &s, hub_cols[q], v);
+                    hub_new[q] = unit_fixed(lp, hub_cols[q]) ? lp->z[hub_cols[q]] : v[0];
+                }
+                for (int64_t q = 0; q < n_hub_cols; q++) {
+                    int64_t u = hub_cols[q];
+                    REAL d = hub_new[q] - lp->z[u];
+                    lp->z[u] = hub_new[q];
+                    hub_new[q] = d;
+                    nnz += col_nnz(lp, u);
+                    updates += 1;
+                }
+            }
             /* (3) tiles of structural units in permutation order, each one synchronous
-             * step of its units (hub tiles have no units left) */
+             * step of its units from r without the pending hub steps (hub tiles have
+             * no units left) */
             thetis_ref_tile_perm(n_struct_tiles, seed, e, perm);
             for (int64_t t = 0; t < n_struct_tiles; t++) {
                 if (hub_tile && hub_tile[perm[t]]) continue;
                 int64_t u0 = perm[t] * 32, u1 = u0 + 32 < n_struct_units ? u0 + 32 : n_struct_units;
                 nnz += step_tile_sync(lp, &s, u0, u1, &updates, nv);
             }
+            /* after the last epoch the pending steps enter r: r = A z - b again */
+            if (hub_cols && e == epochs - 1)
+                for (int64_t q = 0; q < n_hub_cols; q++) col_axpy(lp, hub_cols[q], hub_new[q]);
         } else {
             for (int64_t u = 0; u < lp->U; u++) {
                 if (unit_fixed(lp, u)) continue;

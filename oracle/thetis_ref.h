@@ -96,13 +96,16 @@ double thetis_ref_grad(const ref_lp* lp, float beta, int64_t j);
  * mode 1 = unit-sequential replay of the tile permutation (Alg. 1 one
  *          coordinate at a time, in the async order);
  * mode 2 = plain cyclic sweep;
- * mode 3 = the async reference trajectory (R-6), per epoch: (1) VC / MIS:
- *          the scalar columns of the hub tiles (tiles of 32 structural units
- *          whose columns hold > 512 nonzeros) take one synchronous step;
- *          (2) every slack takes its step (slacks share no row); (3) the tiles
- *          of 32 structural units in permutation order (pi_e over the
- *          structural tiles), each one synchronous step of its units (every
- *          unit steps from the state at the tile's start), hub tiles skipped. */
+ * mode 3 = the async reference trajectory (R-6), per epoch: (1) the hub
+ *          steps pending from the previous epoch enter r, then every slack
+ *          takes its step (slacks share no row); (2) VC / MIS: the scalar
+ *          columns of the hub tiles (tiles of 32 structural units whose columns
+ *          hold > 512 nonzeros) take one synchronous step, z moves and the
+ *          step d stays pending; (3) the tiles of 32 structural units in
+ *          permutation order (pi_e over the structural tiles), each one
+ *          synchronous step of its units (every unit steps from the state at
+ *          the tile's start; r without the pending d), hub tiles skipped.
+ *          After the call's last epoch d enters r (r = A z - b on return). */
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                      int step_rule, ref_stats* st);
 int thetis_ref_objective(const ref_lp* lp, float beta, ref_objective* out);

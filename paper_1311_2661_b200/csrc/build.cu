@@ -2,8 +2,10 @@
 // LP in HBM (CSC with sign-bit coefficients, unique edge rows, costs, bounds), the
 // initial point z0 with r0 = A z0 - b, and max ||a_j||^2 for L_max (Eq. 7).
 //
-//   rows: one per unique undirected non-loop edge (u < v), ordered by (v, u), so
-//   that a vertex's edges to smaller ids form one contiguous run of rows
+//   rows: one per unique undirected non-loop edge (u < v), ordered by
+//   (u >> kRowRangeShift, v, u) (R-17): the rows whose min endpoint lies in one
+//   range of 2^14 ids are contiguous (the hub step accumulates that side in shared
+//   memory), and within a range a vertex's edges to smaller ids are one run
 //   VC  (Eq. 2):   row e = (u < v): x_u + x_v - s_e = 1
 //   MIS (App. B.2):           row e:           x_u + x_v + s_e = 1, max w^T x
 //   MWC (App. B.3): x_v^l at v*k+l, x_e^l at n*k+e*k+l;
@@ -25,10 +27,11 @@ constexpr int T = 256;
 enum Flag { FLAG_BAD_INPUT = 0, FLAG_DUP_TERMINAL = 1, FLAG_BAD_CSC = 2, FLAG_BAD_CSR = 3, FLAG_BAD_BOUNDS = 4 };
 
 // ---------------------------------------------------------------- K1: keys
-__global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ src,
+// key(u < v) = ((u >> kRowRangeShift) n + v) n + u; invalid pairs and self-loops
+// take `sent` (> every key) and sort last
+__global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* __restrict__ src,
                             const int32_t* __restrict__ dst, uint64_t* __restrict__ keys,
                             int32_t* __restrict__ idx, int32_t* flags) {
-    const uint64_t sent = (uint64_t)n * (uint64_t)n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t u = src[i], v = dst[i];
         if (u < 0 || v < 0 || u >= n || v >= n) {
@@ -38,7 +41,7 @@ __global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ sr
             keys[i] = sent; // self-loop: sorts last, dropped
         } else {
             uint64_t a = (uint64_t)(u < v ? u : v), b = (uint64_t)(u < v ? v : u);
-            keys[i] = b * (uint64_t)n + a; // rows in (max, min) order
+            keys[i] = ((a >> kRowRangeShift) * (uint64_t)n + b) * (uint64_t)n + a;
         }
         if (idx) idx[i] = (int32_t)i;
     }
@@ -47,54 +50,50 @@ __global__ void k_make_keys(int64_t E, int64_t n, const int32_t* __restrict__ sr
 __global__ void k_decode_edges(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
-        edges[e] = make_int2((int32_t)(k % (uint64_t)n), (int32_t)(k / (uint64_t)n)); // (min, max)
+        edges[e] = make_int2((int32_t)(k % (uint64_t)n), (int32_t)((k / (uint64_t)n) % (uint64_t)n)); // (min, max)
     }
 }
-// (min endpoint, e) pairs for the stable by-min sort (the scattered incidences)
-__global__ void k_vkeys(int64_t m, const int2* __restrict__ edges, int32_t* __restrict__ vkey, int32_t* __restrict__ eval) {
+// (endpoint, e) pairs for the stable by-endpoint sorts (side 0: min, 1: max)
+__global__ void k_vkeys(int64_t m, const int2* __restrict__ edges, int side, int32_t* __restrict__ vkey,
+                        int32_t* __restrict__ eval) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        vkey[e] = edges[e].x;
+        const int2 uv = edges[e];
+        vkey[e] = side ? uv.y : uv.x;
         eval[e] = (int32_t)e;
     }
 }
-
-// run boundaries of a sorted key sequence: start[key] = first pos, end[key] = last pos + 1
-// rows come in runs of equal max endpoint
-__global__ void k_runs_u(int64_t m, const int2* __restrict__ edges, int32_t* start, int32_t* end) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        int u = edges[e].y;
-        if (e == 0 || edges[e - 1].y != u) start[u] = (int32_t)e;
-        if (e == m - 1 || edges[e + 1].y != u) end[u] = (int32_t)(e + 1);
+// rows per max endpoint: runs of equal max within a warp add with one atomic
+__global__ void k_count_max(int64_t m, const int2* __restrict__ edges, int32_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < m;
+         e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int v = e0 < m ? edges[e0].y : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, v);
+        if (v >= 0 && lane == __ffs(same) - 1) atomicAdd(cnt + v, __popc(same));
     }
 }
+// run boundaries of a sorted key sequence: start[key] = first pos, end[key] = last pos + 1
 __global__ void k_runs_key(int64_t m, const int32_t* __restrict__ key, int32_t* start, int32_t* end) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
         int v = key[p];
         if (p == 0 || key[p - 1] != v) start[v] = (int32_t)p;
-        if (p == m - 1 || key[p + 1] != v) end[v] = (int32_t)(p + 1);
+        if (end && (p == m - 1 || key[p + 1] != v)) end[v] = (int32_t)(p + 1);
     }
 }
-__global__ void k_degrees(int64_t n, const int32_t* us, const int32_t* ue, const int32_t* ls, const int32_t* le,
-                          int64_t* deg) {
+__global__ void k_degrees(int64_t n, const int32_t* cnt_max, const int32_t* ls, const int32_t* le, int64_t* deg) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x)
-        deg[v] = v < n ? (int64_t)(ue[v] - us[v]) + (int64_t)(le[v] - ls[v]) : 0;
+        deg[v] = v < n ? (int64_t)cnt_max[v] + (int64_t)(le[v] - ls[v]) : 0;
 }
-// incidence lists in ascending row order: the run of rows where the vertex is the
-// max endpoint (contiguous, smaller row ids) comes first, then the rows where it is
-// the min endpoint (scattered; stable by-min sort keeps them ascending).
-__global__ void k_fill_lower(int64_t m, const int32_t* __restrict__ vkey, const int32_t* __restrict__ eval,
-                             const int32_t* __restrict__ us, const int32_t* __restrict__ ue,
-                             const int32_t* __restrict__ ls, const int64_t* __restrict__ iptr, int32_t* inc) {
+// incidence lists in ascending row order (R-17): the rows where the vertex is the
+// max endpoint (ranges of smaller ids, then its own) come first, then the rows where
+// it is the min endpoint (all in its own range, after its max run).  Each part comes
+// from a stable by-endpoint sort of the rows; `skip` = count of the first part.
+__global__ void k_fill_part(int64_t m, const int32_t* __restrict__ vkey, const int32_t* __restrict__ eval,
+                            const int32_t* __restrict__ start, const int32_t* __restrict__ skip,
+                            const int64_t* __restrict__ iptr, int32_t* inc) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
         int v = vkey[p];
-        inc[iptr[v] + (ue[v] - us[v]) + (p - ls[v])] = eval[p];
-    }
-}
-__global__ void k_fill_upper(int64_t m, const int2* __restrict__ edges, const int32_t* __restrict__ us,
-                             const int64_t* __restrict__ iptr, int32_t* inc) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        int u = edges[e].y;
-        inc[iptr[u] + (e - us[u])] = (int32_t)e;
+        inc[iptr[v] + (skip ? skip[v] : 0) + (p - start[v])] = eval[p];
     }
 }
 
@@ -338,6 +337,16 @@ __global__ void k_epoch_work(DevLP L, unsigned long long* out) {
         atomicAdd(out + 1, nnz);
     }
 }
+
+// the largest row key + 1 (R-17 key of the pair (n - 2, n - 1), see k_make_keys);
+// graph_keys_fit(n): representable in 64 bits (n up to 2^26 and a bit beyond)
+static unsigned __int128 graph_key_end(int64_t n) {
+    if (n <= 1) return 1;
+    const unsigned __int128 nn = (unsigned __int128)n, u = nn - 2, v = nn - 1;
+    return ((u >> kRowRangeShift) * nn + v) * nn + u + 1;
+}
+bool graph_keys_fit(int64_t n) { return graph_key_end(n) <= (unsigned __int128)UINT64_MAX; }
+uint64_t graph_key_sentinel(int64_t n) { return (uint64_t)graph_key_end(n); }
 
 int bits_for(uint64_t v) {
     int b = 0;
@@ -604,11 +613,13 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     if (mwc) THETIS_TRY(copy_in(lp, t.ew_in, edge_w, (size_t)E * 4));
     if (mwc && t_per_label > 0) THETIS_TRY(copy_in(lp, t.terms, terminals, (size_t)k * t_per_label * 4));
 
-    // ---- K1: canonical keys u*n+v (u < v), sort, unique -> rows
+    // ---- K1: canonical keys (u < v, R-17), sort, unique -> rows
     int64_t m = 0;
+    if (!graph_keys_fit(n))
+        return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "n = %lld: row keys exceed 64 bits", (long long)n);
     if (E > 0) {
-        k_make_keys<<<grid_for(E, T), T, 0, s>>>(E, n, srcd, dstd, t.keys, mwc ? t.idx : nullptr, lp->flags);
-        const uint64_t sent = (uint64_t)n * (uint64_t)n;
+        const uint64_t sent = graph_key_sentinel(n);
+        k_make_keys<<<grid_for(E, T), T, 0, s>>>(E, n, sent, srcd, dstd, t.keys, mwc ? t.idx : nullptr, lp->flags);
         const int end_bit = bits_for(sent);
         size_t cb = t.cub_bytes;
         cub::DoubleBuffer<uint64_t> dk(t.keys, t.keys2);
@@ -646,8 +657,7 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     d.m_edges = m;
     THETIS_TRY(check_cuda(lp, "build: keys"));
 
-    // ---- incidence lists, ascending edge order per vertex: runs of u in row
-    // order, runs of v after a stable (v, e) sort
+    // ---- incidence lists, ascending row order per vertex
     int64_t* iptr = mwc ? t.iptr : (int64_t*)d.colptr;
     int32_t* inc = mwc ? t.inc : (int32_t*)d.rowidx;
     if (n > 0) {
@@ -656,26 +666,28 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
         CUDA_TRY(lp, cudaMemsetAsync(t.ls, 0, (size_t)n * 4, s));
         CUDA_TRY(lp, cudaMemsetAsync(t.le, 0, (size_t)n * 4, s));
     }
-    const int32_t* vsorted = nullptr;
-    const int32_t* esorted = nullptr;
+    // max side: counts now, positions after the by-max sort below; min side: the
+    // by-min sort gives counts and positions
     if (m > 0) {
-        k_runs_u<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, t.ue);
-        k_vkeys<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.vkey, t.eval);
+        k_count_max<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.ue);
+        k_vkeys<<<grid_for(m, T), T, 0, s>>>(m, d.edges, 0, t.vkey, t.eval);
         cub::DoubleBuffer<int32_t> dv(t.vkey, t.vkey2), de(t.eval, t.eval2);
         size_t cb = t.cub_bytes;
         CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(t.cub, cb, dv, de, m, 0, bits_for((uint64_t)n), s));
-        vsorted = dv.Current();
-        esorted = de.Current();
-        k_runs_key<<<grid_for(m, T), T, 0, s>>>(m, vsorted, t.ls, t.le);
-    }
-    k_degrees<<<grid_for(n + 1, T), T, 0, s>>>(n, t.us, t.ue, t.ls, t.le, t.deg);
-    {
-        size_t cb = t.cub_bytes;
+        k_runs_key<<<grid_for(m, T), T, 0, s>>>(m, dv.Current(), t.ls, t.le);
+        k_degrees<<<grid_for(n + 1, T), T, 0, s>>>(n, t.ue, t.ls, t.le, t.deg);
+        cb = t.cub_bytes;
         CUDA_TRY(lp, cub::DeviceScan::ExclusiveSum(t.cub, cb, t.deg, iptr, n + 1, s));
-    }
-    if (m > 0) {
-        k_fill_lower<<<grid_for(m, T), T, 0, s>>>(m, vsorted, esorted, t.us, t.ue, t.ls, iptr, inc);
-        k_fill_upper<<<grid_for(m, T), T, 0, s>>>(m, d.edges, t.us, iptr, inc);
+        k_fill_part<<<grid_for(m, T), T, 0, s>>>(m, dv.Current(), de.Current(), t.ls, t.ue, iptr, inc);
+        k_vkeys<<<grid_for(m, T), T, 0, s>>>(m, d.edges, 1, t.vkey, t.eval);
+        dv = cub::DoubleBuffer<int32_t>(t.vkey, t.vkey2);
+        de = cub::DoubleBuffer<int32_t>(t.eval, t.eval2);
+        cb = t.cub_bytes;
+        CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(t.cub, cb, dv, de, m, 0, bits_for((uint64_t)n), s));
+        k_runs_key<<<grid_for(m, T), T, 0, s>>>(m, dv.Current(), t.us, nullptr);
+        k_fill_part<<<grid_for(m, T), T, 0, s>>>(m, dv.Current(), de.Current(), t.us, nullptr, iptr, inc);
+    } else {
+        CUDA_TRY(lp, cudaMemsetAsync(iptr, 0, (size_t)(n + 1) * 8, s));
     }
     THETIS_TRY(check_cuda(lp, "build: incidence"));
 

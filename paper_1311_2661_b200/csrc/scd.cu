@@ -441,89 +441,55 @@ __device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P
 }
 
 // Hub step (R-6): tiles whose scalar columns hold more than kHeavy nonzeros take
-// one synchronous block step at the start of the epoch.  For VC / MIS (every row
-// = one edge (u, v) with coefficients +1, and a synchronous step with 1/L_max is
-// a descent step) it runs as two coalesced streams over the rows: the gather
-// adds r_e into the (L2-resident) accumulators of the hub endpoints, the update
-// takes the hub steps, the scatter adds the hub steps of both endpoints to r_e
-// with a plain read-modify-write (the hub phase runs alone).
-// The hottest hubs (top kMaxHot by degree) receive ~1e6 min-side additions per epoch;
-// same-address atomics serialise at their L2 slice, so each of them gets kReplicas
-// accumulator copies (spread by warp), folded before the update.
-constexpr int kMaxHot = 8192;
-constexpr int kReplicas = 32;
-constexpr int32_t kHotBit = 1 << 30;  // in row_slot.x: the value is a hot id, not a slot
+// one synchronous step per epoch.  For VC / MIS (every row = one edge (u, v) with
+// coefficients +1) it runs as one stream over the rows plus a small update:
+//   row pass:  r_e += d_u + d_v (the pending hub steps of the previous epoch),
+//              the row's slack step, then r_e into the accumulators D of its hub
+//              endpoints;
+//   update:    z_j -= (grad_j from D_j) / L for every hub column; d_j pending.
+// Rows are grouped by the range of 2^14 ids of their min endpoint (R-17), so one
+// block works on one range at a time: the min side's d and D live in shared
+// memory (no global atomics for that side); the max side comes in runs of equal
+// endpoint inside a range and adds with one atomic per warp run.
+// Accumulators and pending steps are compact, hub-major: slot = 32 hub_id + lane.
+__device__ __forceinline__ float* acc_of(const float2* hv, int32_t slot) { return (float*)hv + 2 * (int64_t)slot; }
+__device__ __forceinline__ float pend_of(const float2* hv, int32_t slot) { return __ldg((const float*)hv + 2 * (int64_t)slot + 1); }
 struct HubCtx {
     int64_t n_heavy;
     const int32_t* heavy_tiles;  // sorted tile ids
     const int32_t* hub_id;       // per structural tile: index in heavy_tiles, or -1
-    const int2* row_slot;        // per row: accumulator slots of (min, max) endpoint, -1 if not a hub;
-                                 // .x = kHotBit | hot id for a hot min endpoint
-    float* buf;                  // compact accumulators, transposed: [lane][hub id] (L2-resident,
-                                 // and the top hubs 0, 1, 2, 4, ... fall in different lines)
-    const int32_t* hot_slot;     // hot id -> slot
-    float* hotbuf;               // [hot id][kReplicas]
-    int64_t n_hot;
+    float2* hv;                  // per slot {D_j (accumulated A^T r), d_j (pending step)}:
+                                 // the max side reads d and adds into D in one sector
+    const int4* items;           // row pass work items {range, row begin, row end, shared}
+    int n_items;
+    unsigned long long* next;    // work item counter
+    const int2* pk;              // per-row keys of the row pass (k_pass_keys)
 };
-__device__ __forceinline__ int32_t plain_slot(const HubCtx& H, int32_t x) {
-    return (x >= 0 && (x & kHotBit)) ? H.hot_slot[x & ~kHotBit] : x;
-}
-__device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int64_t v) {
+__device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int32_t v) {
     const int32_t h = H.hub_id[v >> 5];
-    return h < 0 ? -1 : (int32_t)((v & 31) * H.n_heavy + h);
+    return h < 0 ? -1 : h * 32 + (v & 31);
 }
 
 __global__ void k_hub_ids(int64_t n_heavy, const int32_t* heavy_tiles, int32_t* hub_id) {
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < n_heavy; h += (int64_t)gridDim.x * blockDim.x)
         hub_id[heavy_tiles[h]] = (int32_t)h;
 }
-__global__ void k_row_slots(DevLP L, HubCtx H, const int32_t* hot_of_slot, int2* row_slot) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
-        const int2 uv = L.edges[e];
-        int32_t x = hub_slot(H, uv.x);
-        if (x >= 0 && hot_of_slot[x] >= 0) x = kHotBit | hot_of_slot[x];
-        row_slot[e] = make_int2(x, hub_slot(H, uv.y));
-    }
-}
-// log2-degree histogram of the hub columns, to pick the hot threshold
-__global__ void k_hub_deg_hist(DevLP L, HubCtx H, unsigned long long* hist) {
-    __shared__ unsigned long long sh[64];
-    if (threadIdx.x < 64) sh[threadIdx.x] = 0;
-    __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H.n_heavy * 32; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
-        if (j >= L.n_scalar) continue;
-        const int64_t d = L.colptr[j + 1] - L.colptr[j];
-        atomicAdd(sh + (d > 0 ? 63 - __clzll(d) : 0), 1ull);
-    }
-    __syncthreads();
-    if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
-}
-__global__ void k_hot_assign(DevLP L, HubCtx H, int64_t thr, int64_t hot_cap, int32_t* hot_of_slot,
-                             int32_t* hot_slot, unsigned long long* count) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < H.n_heavy * 32; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t h = i >> 5, lane = i & 31;
-        const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
-        const int32_t slot = (int32_t)(lane * H.n_heavy + h);
-        hot_of_slot[slot] = -1;
-        if (j >= L.n_scalar || L.colptr[j + 1] - L.colptr[j] < thr) continue;
-        const unsigned long long id = atomicAdd(count, 1ull);
-        if (id < (unsigned long long)hot_cap) {
-            hot_of_slot[slot] = (int32_t)id;
-            hot_slot[id] = slot;
+// first row of every range of min endpoints (rows are sorted by range): lower bound
+__global__ void k_range_starts(DevLP L, int64_t n_ranges, int32_t* start) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= n_ranges; g += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = L.m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)(L.edges[mid].x >> kRowRangeShift) < g) lo = mid + 1;
+            else hi = mid;
         }
+        start[g] = (int32_t)lo;
     }
-}
-// hot replicas -> the plain accumulators (after the gather, before the update)
-__global__ void k_hot_fold(HubCtx H) {
-    const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (h >= H.n_hot) return;
-    float s = 0.0f;
-    for (int q = 0; q < kReplicas; q++) s += H.hotbuf[h * kReplicas + q];
-    H.buf[H.hot_slot[h]] += s;
 }
 
-constexpr int kRowsPerThread = 8;
+constexpr int kPassThreads = 1024;             // one block per SM, shared d / D of one range
+constexpr int64_t kItemRows = 1 << 17;         // rows per work item
+constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side through global memory
 
 // v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
 // not a hub); add the warp's run segments with one atomic each.  Fast path when
@@ -547,92 +513,141 @@ __device__ __forceinline__ void add_max_side(float* acc, int key, float val, int
     const int prev = __shfl_up_sync(0xffffffffu, key, 1);
     if (key >= 0 && (lane == 0 || prev != key)) atomicAdd(acc + key, sv);
 }
-// (1a) r_e into the accumulators of the hub endpoints: the min endpoint by an
-// atomic per row, the max endpoint by add_max_side.  kRowsPerThread rows per
-// thread, all loads issued before any atomic.
-__global__ void __launch_bounds__(256) k_hub_rows_gather(DevLP L, HubCtx H, float* acc) {
+
+// per-row keys of the row pass, built once per solve: .x = the min endpoint's
+// index in its range's shared arrays (rows of shared items) or its global slot
+// (other rows), .y = the max endpoint's global slot; -1 = not a hub column
+__global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range_shared, int2* __restrict__ pk) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int2 uv = L.edges[e];
+        const int32_t g = uv.x >> kRowRangeShift;
+        int32_t su = hub_slot(H, uv.x);
+        if (su >= 0 && range_shared[g]) su = uv.x - (g << kRowRangeShift);
+        pk[e] = make_int2(su, hub_slot(H, uv.y));
+    }
+}
+
+// The row pass (kSlack) or, after a call's last epoch, the application of the
+// pending steps alone (!kSlack).  Persistent blocks take work items in order; an
+// item with `shared` set stages d of its range in shared memory and accumulates
+// the min side of D there, flushed with one atomic per hub column at the end.
+// kAnchor: the LP has anchors (zbar / ubar), else both are zero.  The slack step
+// is slack_new<true> written out for graph rows (sigma = sg for every row).
+constexpr int kPassRows = 4;
+constexpr size_t kPassSmem = 2 * kRowRange * sizeof(float);
+template <bool kSlack, bool kAnchor>
+__global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepParams P, HubCtx H, int apply) {
+    extern __shared__ float smem[];
+    float* s_pend = smem;               // d of the range's columns
+    float* s_acc = smem + kRowRange;    // D (min side) of the range's columns
+    __shared__ int32_t s_hub[kRowRange / 32];
+    __shared__ int s_it;
     const int lane = threadIdx.x & 31;
-    const int64_t span = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
-         e0 += kRowsPerThread * span) {
-        int2 sl[kRowsPerThread];
-        float rv[kRowsPerThread];
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) {
-            const int64_t e = e0 + q * span;
-            sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
-            rv[q] = (sl[q].x >= 0 || sl[q].y >= 0) ? ld_cg(L.r + e) : 0.0f;
-        }
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) {
-            if (sl[q].x >= 0) {
-                if (sl[q].x & kHotBit)
-                    atomicAdd(H.hotbuf + (int64_t)(sl[q].x & ~kHotBit) * kReplicas + ((threadIdx.x >> 5) + blockIdx.x) % kReplicas, rv[q]);
-                else
-                    atomicAdd(acc + sl[q].x, rv[q]);
+    const float sg = row_sigma(L, 0);
+    const float invLs = unit_invL(P, 1.0);
+    const float beta = P.beta, inv_beta = P.inv_beta;
+    float* __restrict__ r = L.r;
+    float* __restrict__ zs = L.z + L.n_s;
+    const int2* __restrict__ pk = H.pk;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_it = (int)atomicAdd(H.next, 1ull);
+        __syncthreads();
+        const int it = s_it;
+        if (it >= H.n_items) return;
+        const int4 w = H.items[it];
+        const int32_t base = w.x << kRowRangeShift;
+        const bool sh = w.w != 0;
+        if (sh) {
+            for (int t = threadIdx.x; t < kRowRange / 32; t += blockDim.x)
+                s_hub[t] = (int64_t)base + t * 32 < L.n_scalar ? H.hub_id[(base >> 5) + t] : -1;
+            __syncthreads();
+            for (int i = threadIdx.x; i < kRowRange; i += blockDim.x) {
+                const int32_t h = s_hub[i >> 5];
+                s_pend[i] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
+                s_acc[i] = 0.0f;
             }
-            add_max_side(acc, sl[q].y, rv[q], lane);
+            __syncthreads();
+        }
+        for (int64_t e0 = w.y + threadIdx.x; e0 - lane < w.z; e0 += kPassRows * (int64_t)blockDim.x) {
+            int2 key[kPassRows];
+            float r0[kPassRows], z[kPassRows];
+#pragma unroll
+            for (int q = 0; q < kPassRows; q++) {
+                const int64_t e = e0 + q * (int64_t)blockDim.x;
+                const bool take = e < w.z;
+                key[q] = take ? __ldcs(pk + e) : make_int2(-1, -1);
+                r0[q] = take ? __ldcs(r + e) : 0.0f;
+                if (kSlack) z[q] = take ? __ldcs(zs + e) : 0.0f;
+            }
+            float rv[kPassRows];
+#pragma unroll
+            for (int q = 0; q < kPassRows; q++) {
+                const int64_t e = e0 + q * (int64_t)blockDim.x;
+                const bool take = e < w.z;
+                float du = 0.0f, dv = 0.0f;
+                if (apply) {
+                    if (key[q].x >= 0) du = sh ? s_pend[key[q].x] : pend_of(H.hv, key[q].x);
+                    if (key[q].y >= 0) dv = pend_of(H.hv, key[q].y);
+                }
+                const float delta = __fadd_rn(du, dv);
+                float x = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
+                if (kSlack && take) {
+                    // slack_new<true>: D = sigma r, g = -ua + beta D + (z - zbar) / beta
+                    float ua = 0.0f, zb = 0.0f;
+                    if (kAnchor) {
+                        if (L.ubar) ua = __fadd_rn(0.0f, sg < 0.0f ? -L.ubar[e] : L.ubar[e]);
+                        if (L.zbar) zb = L.zbar[L.n_s + e];
+                    }
+                    const float D = __fadd_rn(0.0f, sg < 0.0f ? -x : x);
+                    float g = __fsub_rn(0.0f, ua);
+                    g = __fadd_rn(g, __fmul_rn(beta, D));
+                    g = __fadd_rn(g, __fmul_rn(__fsub_rn(z[q], zb), inv_beta));
+                    float t = __fsub_rn(z[q], __fmul_rn(g, invLs));
+                    t = t < 0.0f ? 0.0f : t;
+                    const float d = __fsub_rn(t, z[q]);
+                    if (d != 0.0f) {
+                        x = __fadd_rn(x, sg < 0.0f ? -d : d);
+                        __stcs(zs + e, t);
+                    }
+                }
+                if (take && x != r0[q]) __stcs(r + e, x);
+                rv[q] = x;
+            }
+            if (kSlack) {
+#pragma unroll
+                for (int q = 0; q < kPassRows; q++) {
+                    if (key[q].x >= 0) {
+                        if (sh) atomicAdd(s_acc + key[q].x, rv[q]);
+                        else atomicAdd(acc_of(H.hv, key[q].x), rv[q]);
+                    }
+                    add_max_side((float*)H.hv, key[q].y >= 0 ? 2 * key[q].y : -1, rv[q], lane);
+                }
+            }
+        }
+        if (kSlack && sh) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < kRowRange; i += blockDim.x) {
+                const int32_t h = s_hub[i >> 5];
+                const float a = s_acc[i];
+                if (h >= 0 && a != 0.0f) atomicAdd(acc_of(H.hv, h * 32 + (i & 31)), a);
+            }
         }
     }
 }
-// the hub steps: buf[j] holds D_j on entry and the step d_j on exit
+// the hub steps from the accumulated A^T r: z_j takes the step, d_j becomes
+// pending (applied to r by the next row pass)
 __global__ void k_hub_update(DevLP L, StepParams P, HubCtx H) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= H.n_heavy * 32) return;
-    const int64_t h = i >> 5, lane = i & 31;  // consecutive threads: consecutive columns
-    const int64_t j = (int64_t)H.heavy_tiles[h] * 32 + lane;
-    if (j >= L.n_scalar) return;
-    const int64_t slot = lane * H.n_heavy + h;
+    const int64_t j = (int64_t)H.heavy_tiles[i >> 5] * 32 + (i & 31);
+    if (j >= L.n_scalar) { H.hv[i] = make_float2(0.0f, 0.0f); return; }
     float z = L.z[j];
-    float g = grad_fast(c_int(L, j), ua_of(L, j), H.buf[slot], z, zbar_of(L, j), P.beta, P.inv_beta);
+    float g = grad_fast(c_int(L, j), ua_of(L, j), H.hv[i].x, z, zbar_of(L, j), P.beta, P.inv_beta);
     float invL = P.rule == THETIS_STEP_LMAX ? P.invLmax : unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
-    H.buf[slot] = __fsub_rn(zn, z);
-}
-// (2) fused with the end of (1): per row, add the hub steps of both endpoints to
-// r_e, then take the row's slack step from the fresh r_e (VC / MIS: row e has
-// slack column n + e); one read-modify-write of r and s per row
-__global__ void __launch_bounds__(256) k_rows_hub_slack(DevLP L, StepParams P, HubCtx H) {
-    const int lane = threadIdx.x & 31;
-    const int64_t span = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < L.m;
-         e0 += kRowsPerThread * span) {
-        int2 sl[kRowsPerThread];
-        bool take[kRowsPerThread];
-        float r0[kRowsPerThread], z[kRowsPerThread];
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) {
-            const int64_t e = e0 + q * span;
-            sl[q] = e < L.m ? H.row_slot[e] : make_int2(-1, -1);
-            take[q] = e < L.m;
-            r0[q] = take[q] ? L.r[e] : 0.0f;
-            z[q] = take[q] ? L.z[L.n_s + e] : 0.0f;
-        }
-        float rv[kRowsPerThread], du[kRowsPerThread], dv[kRowsPerThread];
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) { // all hub-step loads in flight together
-            du[q] = take[q] && sl[q].x >= 0 ? H.buf[plain_slot(H, sl[q].x)] : 0.0f;
-            dv[q] = take[q] && sl[q].y >= 0 ? H.buf[sl[q].y] : 0.0f;
-        }
-#pragma unroll
-        for (int q = 0; q < kRowsPerThread; q++) {
-            const int64_t e = e0 + q * span;
-            const float delta = __fadd_rn(du[q], dv[q]);
-            rv[q] = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
-            if (take[q]) {
-                const int64_t j = L.n_s + e;
-                const float sig = row_sigma(L, e);
-                const float zn = slack_new<true>(L, P, e, j, sig, rv[q], z[q]);
-                const float d = __fsub_rn(zn, z[q]);
-                if (d != 0.0f) {
-                    rv[q] = __fadd_rn(rv[q], sig < 0.0f ? -d : d);
-                    L.z[j] = zn;
-                }
-                if (rv[q] != r0[q]) L.r[e] = rv[q];
-            }
-        }
-    }
+    H.hv[i] = make_float2(0.0f, __fsub_rn(zn, z));  // D restarts at 0 for the next row pass
 }
 // (2) without a hub step: the slack sweep
 __global__ void __launch_bounds__(256) k_slack_sweep(DevLP L, StepParams P) {
@@ -766,6 +781,20 @@ static int64_t async_workers(int64_t n_tiles) {
     return w < 1 ? 1 : w;
 }
 
+// persistent grid of the row pass: one block per SM (shared d / D of one range)
+static int64_t pass_blocks() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_rows_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+        cudaFuncSetAttribute(k_rows_pass<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+        cudaFuncSetAttribute(k_rows_pass<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+    }
+    return sms;
+}
+
 // hub tiles (VC / MIS only, see the hub step): per-tile flags and the sorted
 // list, cached per LP in the persistent `heavy` region (8 n_tiles + 8 bytes:
 // flags in the first n_tiles bytes, then the list)
@@ -823,6 +852,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     AsyncCtx AC{};
     HubCtx H{};
     int64_t blocks = 1, hub_blocks = 1, workers = 1;
+    bool anchored = false;
     int batch = 1;
     if (mode != THETIS_MODE_DETERMINISTIC) {
         THETIS_TRY(ensure_heavy(lp));
@@ -834,43 +864,56 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         batch = blocks >= 128 ? kBatch : 1;
         Carver C(lp->temp);
         AC.next = C.take<unsigned long long>(32 * (int64_t)AC.streams);
-        int2* row_slot = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
         int32_t* hub_id = C.take<int32_t>(n_tiles);
-        H.row_slot = row_slot;
         H.hub_id = hub_id;
-        H.buf = C.take<float>(H.n_heavy * 32);
-        // hot replicas only when there are hubs (the buffer doubles as the degree histogram)
-        const int64_t hot_cap = H.n_heavy * 32 < kMaxHot ? H.n_heavy * 32 : kMaxHot;
-        int32_t* hot_of_slot = C.take<int32_t>(H.n_heavy * 32);
-        int32_t* hot_slot = C.take<int32_t>(hot_cap);
-        H.hot_slot = hot_slot;
-        H.hotbuf = C.take<float>(H.n_heavy > 0 ? (hot_cap * kReplicas > 160 ? hot_cap * kReplicas : 160) : 1);
+        H.hv = C.take<float2>(H.n_heavy * 32);
+        H.next = C.take<unsigned long long>(32 * 2);
+        const int64_t n_ranges = (L.n_scalar + kRowRange - 1) / kRowRange;
+        int32_t* rstart = C.take<int32_t>(n_ranges + 1);
+        const int64_t max_items = L.m / kItemRows + 2 * n_ranges + 2;
+        int4* items = C.take<int4>(H.n_heavy > 0 ? max_items : 1);
+        H.items = items;
+        uint8_t* range_shared = C.take<uint8_t>(n_ranges + 1);
+        int2* pk = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
+        H.pk = pk;
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
         if (H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
+            CUDA_TRY(lp, cudaMemsetAsync(H.hv, 0, (size_t)H.n_heavy * 32 * 8, s));
             k_hub_ids<<<grid_for(H.n_heavy, 256), 256, 0, s>>>(H.n_heavy, H.heavy_tiles, hub_id);
-            // hot hubs: the smallest power-of-two degree threshold with <= kMaxHot above it
-            std::vector<unsigned long long> hh(64, 0);
-            unsigned long long* dhist = (unsigned long long*)H.hotbuf; // scratch before use
-            CUDA_TRY(lp, cudaMemsetAsync(dhist, 0, 64 * 8 + 8, s));
-            k_hub_deg_hist<<<grid_for(H.n_heavy * 32, 256), 256, 0, s>>>(L, H, dhist);
-            CUDA_TRY(lp, cudaMemcpyAsync(hh.data(), dhist, 64 * 8, cudaMemcpyDeviceToHost, s));
+            // work items of the row pass: ranges of min endpoints, split into chunks
+            // of kItemRows; consecutive small ranges merge into one global-memory item
+            k_range_starts<<<grid_for(n_ranges + 1, 256), 256, 0, s>>>(L, n_ranges, rstart);
+            std::vector<int32_t> hs(n_ranges + 1);
+            CUDA_TRY(lp, cudaMemcpyAsync(hs.data(), rstart, (size_t)(n_ranges + 1) * 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));
-            int b = 63;
-            unsigned long long above = 0;
-            while (b > 0 && above + hh[b] <= (unsigned long long)hot_cap) above += hh[b--];
-            const int64_t thr = (int64_t)1 << (b + 1);
-            CUDA_TRY(lp, cudaMemsetAsync(dhist, 0, 8, s));
-            k_hot_assign<<<grid_for(H.n_heavy * 32, 256), 256, 0, s>>>(L, H, thr, hot_cap, hot_of_slot, hot_slot, dhist);
-            unsigned long long nh = 0;
-            CUDA_TRY(lp, cudaMemcpyAsync(&nh, dhist, 8, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(lp, cudaStreamSynchronize(s));
-            H.n_hot = nh < (unsigned long long)hot_cap ? (int64_t)nh : hot_cap;
-            k_row_slots<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, hot_of_slot, row_slot);
+            std::vector<int4> it;
+            std::vector<uint8_t> rsh(n_ranges + 1, 0);
+            for (int64_t g = 0; g < n_ranges; g++) {
+                const int32_t b0 = hs[g], b1 = hs[g + 1];
+                if (b1 <= b0) continue;
+                if (b1 - b0 >= kSharedMinRows) {
+                    rsh[g] = 1;
+                    for (int64_t p = b0; p < b1; p += kItemRows)
+                        it.push_back(make_int4((int)g, (int)p, (int)(p + kItemRows < b1 ? p + kItemRows : b1), 1));
+                } else if (!it.empty() && it.back().w == 0 && it.back().z == b0 && b1 - it.back().y <= kItemRows) {
+                    it.back().z = b1;
+                } else {
+                    it.push_back(make_int4((int)g, b0, b1, 0));
+                }
+            }
+            if ((int64_t)it.size() > max_items) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "row pass items");
+            H.n_items = (int)it.size();
+            if (!it.empty())
+                CUDA_TRY(lp, cudaMemcpyAsync(items, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(lp, cudaMemcpyAsync(range_shared, rsh.data(), rsh.size(), cudaMemcpyHostToDevice, s));
+            k_pass_keys<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, range_shared, pk);
+            CUDA_TRY(lp, cudaStreamSynchronize(s));  // `it`, `rsh` are pageable host memory
         }
         AC.n_tiles = n_tiles;
         AC.heavy_limit = hub_step_enabled(L) ? kHeavy : INT64_MAX;
-        hub_blocks = grid_for(L.m, 256, 148 * 8);
+        hub_blocks = pass_blocks();
+        anchored = L.zbar != nullptr || L.ubar != nullptr;
     }
     const bool timed = st != nullptr;
     if (timed) {
@@ -892,12 +935,10 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             // (1) hub step + (2) slack sweep, fused; or (2) alone
             if (H.n_heavy > 0) {
                 const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
-                CUDA_TRY(lp, cudaMemsetAsync(H.buf, 0, (size_t)H.n_heavy * 32 * 4, s));
-                if (H.n_hot > 0) CUDA_TRY(lp, cudaMemsetAsync(H.hotbuf, 0, (size_t)H.n_hot * kReplicas * 4, s));
-                k_hub_rows_gather<<<(unsigned)hub_blocks, 256, 0, s>>>(L, H, H.buf);
-                if (H.n_hot > 0) k_hot_fold<<<(unsigned)((H.n_hot + 255) / 256), 256, 0, s>>>(H);
+                CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
+                if (anchored) k_rows_pass<true, true><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0);
+                else k_rows_pass<true, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
-                k_rows_hub_slack<<<(unsigned)hub_blocks, 256, 0, s>>>(L, P, H);
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
             }
@@ -907,6 +948,11 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 AC.K = make_perm_keys(n_tiles, seed, e);
                 k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
+        }
+        // the last epoch's hub steps are still pending: apply them, r = A z - b again
+        if (e == epochs - 1 && mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
+            CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
+            k_rows_pass<false, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, 1);
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));
     }

@@ -12,6 +12,8 @@
 namespace thetis {
 
 constexpr int kTile = 32;          // units per async tile (R-6)
+constexpr int kRowRangeShift = 14; // graph LP rows grouped by min endpoint >> 14 (R-17)
+constexpr int kRowRange = 1 << kRowRangeShift;
 constexpr int kMaxK = 32;          // max simplex block size
 constexpr uint32_t kSignBit = 0x80000000u;
 constexpr uint32_t kRowMask = 0x7FFFFFFFu;

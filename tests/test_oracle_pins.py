@@ -258,6 +258,25 @@ def test_maintained_residual_equals_recomputed():
         assert lp.objective(10.0)["drift_inf"] < 1e-12
 
 
+def test_graph_row_order_spans_ranges():
+    # R-17: rows sorted by (min >> 14, max, min); ids spread over four 2^14 ranges so the
+    # grouping by the min endpoint's range differs from a plain (max, min) order.  Each
+    # column lists its rows in ascending row order.
+    n = 4 << 14
+    src, dst = small_graph(n, 3000, 21)
+    edges = bf.unique_edges(n, src, dst)
+    lp = RefLP.graph(VC, n, src, dst, vertex_w=np.ones(n, np.float32))
+    eu, ev = lp.edges()
+    want = sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
+    assert want != sorted(edges, key=lambda e: (e[1], e[0]))
+    assert list(zip(eu.tolist(), ev.tolist())) == want
+    colptr, rowidx, _ = lp.csc()
+    for v in range(0, n, 97):
+        rows = rowidx[colptr[v]:colptr[v + 1]]
+        assert (np.diff(rows) > 0).all()
+        assert sorted(rows.tolist()) == [i for i, (a, b) in enumerate(want) if v in (a, b)]
+
+
 def test_graph_encoding_counts():
     # VC/MIS: one row per unique undirected non-loop edge, 2 structural nnz + 1 slack per row
     # (Fig. 3 NNZ:PV ~ 3:1); MWC: 2km rows, 6km structural nnz, 2km slacks
@@ -267,7 +286,7 @@ def test_graph_encoding_counts():
     lp = RefLP.graph(VC, 30, src, dst, vertex_w=w)
     assert lp.m == len(edges) and lp.nnz_struct == 2 * len(edges) and lp.n_ineq == len(edges)
     eu, ev = lp.edges()
-    assert list(zip(eu.tolist(), ev.tolist())) == sorted(edges, key=lambda e: (e[1], e[0]))
+    assert list(zip(eu.tolist(), ev.tolist())) == sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
     b, sense, c = lp.rows()
     assert (b == 1).all() and (sense == oracle.SENSE_GE).all()
     lpm = RefLP.graph(MIS, 30, src, dst, vertex_w=w)
