@@ -27,8 +27,9 @@ constexpr int T = 256;
 enum Flag { FLAG_BAD_INPUT = 0, FLAG_DUP_TERMINAL = 1, FLAG_BAD_CSC = 2, FLAG_BAD_CSR = 3, FLAG_BAD_BOUNDS = 4 };
 
 // ---------------------------------------------------------------- K1: keys
-// key(u < v) = ((u >> kRowRangeShift) n + v) n + u; invalid pairs and self-loops
-// take `sent` (> every key) and sort last
+// key(u < v) = ((u >> kRowRangeShift) n + v) 2^kRowRangeShift + (u mod 2^kRowRangeShift):
+// (range of u, v, u) in 2 log2(n) bits; invalid pairs and self-loops take `sent`
+// (> every key) and sort last
 __global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* __restrict__ src,
                             const int32_t* __restrict__ dst, uint64_t* __restrict__ keys,
                             int32_t* __restrict__ idx, int32_t* flags) {
@@ -41,7 +42,7 @@ __global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* 
             keys[i] = sent; // self-loop: sorts last, dropped
         } else {
             uint64_t a = (uint64_t)(u < v ? u : v), b = (uint64_t)(u < v ? v : u);
-            keys[i] = ((a >> kRowRangeShift) * (uint64_t)n + b) * (uint64_t)n + a;
+            keys[i] = ((((a >> kRowRangeShift) * (uint64_t)n + b)) << kRowRangeShift) | (a & (kRowRange - 1));
         }
         if (idx) idx[i] = (int32_t)i;
     }
@@ -50,7 +51,9 @@ __global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* 
 __global__ void k_decode_edges(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
-        edges[e] = make_int2((int32_t)(k % (uint64_t)n), (int32_t)((k / (uint64_t)n) % (uint64_t)n)); // (min, max)
+        const uint64_t gv = k >> kRowRangeShift;    // g n + max
+        const uint64_t g = gv / (uint64_t)n;
+        edges[e] = make_int2((int32_t)((g << kRowRangeShift) | (k & (kRowRange - 1))), (int32_t)(gv - g * (uint64_t)n));
     }
 }
 // (endpoint, e) pairs for the stable by-endpoint sorts (side 0: min, 1: max)
@@ -339,11 +342,11 @@ __global__ void k_epoch_work(DevLP L, unsigned long long* out) {
 }
 
 // the largest row key + 1 (R-17 key of the pair (n - 2, n - 1), see k_make_keys);
-// graph_keys_fit(n): representable in 64 bits (n up to 2^26 and a bit beyond)
+// graph_keys_fit(n): representable in 64 bits
 static unsigned __int128 graph_key_end(int64_t n) {
     if (n <= 1) return 1;
     const unsigned __int128 nn = (unsigned __int128)n, u = nn - 2, v = nn - 1;
-    return ((u >> kRowRangeShift) * nn + v) * nn + u + 1;
+    return ((((u >> kRowRangeShift) * nn + v)) << kRowRangeShift) + (u & (kRowRange - 1)) + 1;
 }
 bool graph_keys_fit(int64_t n) { return graph_key_end(n) <= (unsigned __int128)UINT64_MAX; }
 uint64_t graph_key_sentinel(int64_t n) { return (uint64_t)graph_key_end(n); }
