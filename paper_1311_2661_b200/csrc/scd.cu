@@ -494,13 +494,13 @@ constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side throu
 // v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
 // not a hub); add the warp's run segments with one atomic each.  Fast path when
 // the whole warp is one run.
-__device__ __forceinline__ void add_max_side(float* acc, int key, float val, int lane) {
+__device__ __forceinline__ void add_max_side(float* acc, int key, float val, int lane, bool skip = false) {
     const int k0 = __shfl_sync(0xffffffffu, key, 0);
     if (__all_sync(0xffffffffu, key == k0)) {
         if (k0 < 0) return;
 #pragma unroll
         for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        if (lane == 0) atomicAdd(acc + k0, val);
+        if (lane == 0 && !skip) atomicAdd(acc + k0, val);
         return;
     }
     float sv = key >= 0 ? val : 0.0f;
@@ -511,7 +511,7 @@ __device__ __forceinline__ void add_max_side(float* acc, int key, float val, int
         if (lane + o < 32 && k2 == key) sv += x;
     }
     const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-    if (key >= 0 && (lane == 0 || prev != key)) atomicAdd(acc + key, sv);
+    if (key >= 0 && (lane == 0 || prev != key) && !skip) atomicAdd(acc + key, sv);
 }
 
 // per-row keys of the row pass, built once per solve: .x = the min endpoint's
@@ -534,12 +534,27 @@ __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range
 // kAnchor: the LP has anchors (zbar / ubar), else both are zero.  The slack step
 // is slack_new<true> written out for graph rows (sigma = sg for every row).
 constexpr int kPassRows = 4;
-constexpr size_t kPassSmem = 2 * kRowRange * sizeof(float);
+// shared memory: d of the range (float) and the min side of D as 64-bit fixed point
+// (scale 2^kFixShift) split into unsigned low / signed high words, so that the
+// additions are native integer shared atomics (a float add is a CAS loop)
+constexpr size_t kPassSmem = 3 * kRowRange * sizeof(float);
+constexpr int kFixShift = 24;
+__device__ __forceinline__ void fix_add(uint32_t* lo, int32_t* hi, int i, float x) {
+    const long long v = __float2ll_rn(__fmul_rn(x, (float)(1 << kFixShift)));
+    const uint32_t l = (uint32_t)v;
+    const uint32_t old = atomicAdd(lo + i, l);
+    const int32_t h = (int32_t)(v >> 32) + (old + l < old ? 1 : 0);
+    if (h) atomicAdd(hi + i, h);
+}
+__device__ __forceinline__ float fix_value(uint32_t lo, int32_t hi) {
+    return (float)((double)(((long long)hi << 32) | lo) * (1.0 / (double)(1 << kFixShift)));
+}
 template <bool kSlack, bool kAnchor>
-__global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepParams P, HubCtx H, int apply) {
+__global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepParams P, HubCtx H, int apply, int exp) {
     extern __shared__ float smem[];
-    float* s_pend = smem;               // d of the range's columns
-    float* s_acc = smem + kRowRange;    // D (min side) of the range's columns
+    float* s_pend = smem;                                    // d of the range's columns
+    uint32_t* s_lo = (uint32_t*)(smem + kRowRange);          // D (min side), fixed point
+    int32_t* s_hi = (int32_t*)(smem + 2 * kRowRange);
     __shared__ int32_t s_hub[kRowRange / 32];
     __shared__ int s_it;
     const int lane = threadIdx.x & 31;
@@ -565,7 +580,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             for (int i = threadIdx.x; i < kRowRange; i += blockDim.x) {
                 const int32_t h = s_hub[i >> 5];
                 s_pend[i] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
-                s_acc[i] = 0.0f;
+                s_lo[i] = 0u;
+                s_hi[i] = 0;
             }
             __syncthreads();
         }
@@ -588,7 +604,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                 float du = 0.0f, dv = 0.0f;
                 if (apply) {
                     if (key[q].x >= 0) du = sh ? s_pend[key[q].x] : pend_of(H.hv, key[q].x);
-                    if (key[q].y >= 0) dv = pend_of(H.hv, key[q].y);
+                    if (key[q].y >= 0 && !(exp & 4)) dv = pend_of(H.hv, key[q].y);
                 }
                 const float delta = __fadd_rn(du, dv);
                 float x = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
@@ -617,11 +633,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             if (kSlack) {
 #pragma unroll
                 for (int q = 0; q < kPassRows; q++) {
-                    if (key[q].x >= 0) {
-                        if (sh) atomicAdd(s_acc + key[q].x, rv[q]);
+                    if (key[q].x >= 0 && !(exp & 2)) {
+                        if (sh) fix_add(s_lo, s_hi, key[q].x, rv[q]);
                         else atomicAdd(acc_of(H.hv, key[q].x), rv[q]);
                     }
-                    add_max_side((float*)H.hv, key[q].y >= 0 ? 2 * key[q].y : -1, rv[q], lane);
+                    if (!(exp & 1)) add_max_side((float*)H.hv, key[q].y >= 0 ? 2 * key[q].y : -1, rv[q], lane, exp & 8);
                 }
             }
         }
@@ -629,8 +645,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             __syncthreads();
             for (int i = threadIdx.x; i < kRowRange; i += blockDim.x) {
                 const int32_t h = s_hub[i >> 5];
-                const float a = s_acc[i];
-                if (h >= 0 && a != 0.0f) atomicAdd(acc_of(H.hv, h * 32 + (i & 31)), a);
+                const uint32_t lo = s_lo[i];
+                const int32_t hi = s_hi[i];
+                if (h >= 0 && (lo | (uint32_t)hi)) atomicAdd(acc_of(H.hv, h * 32 + (i & 31)), fix_value(lo, hi));
             }
         }
     }
@@ -835,6 +852,7 @@ static int ensure_heavy(thetis_lp* lp) {
     return check_cuda(lp, "heavy tiles");
 }
 
+static int g_exp = getenv("THETIS_EXP") ? atoi(getenv("THETIS_EXP")) : 0;
 int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                  thetis_solve_stats* st) {
     const DevLP& L = lp->d;
@@ -936,8 +954,8 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (H.n_heavy > 0) {
                 const unsigned hb = (unsigned)((H.n_heavy * 32 + 255) / 256);
                 CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
-                if (anchored) k_rows_pass<true, true><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0);
-                else k_rows_pass<true, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0);
+                if (anchored) k_rows_pass<true, true><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0, 0);
+                else k_rows_pass<true, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0, g_exp);
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
@@ -952,7 +970,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         // the last epoch's hub steps are still pending: apply them, r = A z - b again
         if (e == epochs - 1 && mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
-            k_rows_pass<false, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, 1);
+            k_rows_pass<false, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, 1, 0);
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));
     }
