@@ -312,6 +312,11 @@ static int cmp_keyed(const void* a, const void* b) {
     if (x->key != y->key) return x->key < y->key ? -1 : 1;
     return x->idx < y->idx ? -1 : (x->idx > y->idx);
 }
+static int cmp_plain_key(const void* a, const void* b) { /* (v, u); keys are unique here */
+    const keyed_edge* x = (const keyed_edge*)a;
+    const keyed_edge* y = (const keyed_edge*)b;
+    return x->key < y->key ? -1 : (x->key > y->key);
+}
 
 int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_edges,
                               const int32_t* src, const int32_t* dst, const float* vertex_w,
@@ -327,7 +332,8 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
         if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) return REF_INVALID_ARG;
 
     /* canonicalise (u < v), drop self-loops, sort by (u >> 14, v, u), keep the
-     * first occurrence of each pair: the row order (R-17) */
+     * first occurrence of each pair; then the hub partition below: the row order
+     * (R-17) */
     keyed_edge* ke = (keyed_edge*)xcalloc(n_edges, sizeof(keyed_edge));
     int64_t cnt = 0;
     for (int64_t e = 0; e < n_edges; e++) {
@@ -342,6 +348,29 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     int64_t me = 0;
     for (int64_t t = 0; t < cnt; t++)
         if (t == 0 || ke[t].key != ke[t - 1].key) ke[me++] = ke[t];
+    {
+        /* R-17: the rows whose larger endpoint lies in a hub tile (VC / MIS: a tile
+         * of 32 vertices with more than HUB_NNZ incidences) keep this order; the
+         * others follow, sorted by (v, u) */
+        int64_t n_tiles = (n + 31) / 32;
+        int64_t* tnz = (int64_t*)xcalloc(n_tiles + 1, sizeof(int64_t));
+        for (int64_t e = 0; e < me; e++) {
+            tnz[(ke[e].key & 0xFFFFFFFFu) >> 5]++;
+            tnz[(ke[e].key >> 32) >> 5]++;
+        }
+        int hubs = problem == PROB_VC || problem == PROB_MIS;
+        keyed_edge* ord = (keyed_edge*)xcalloc(me + 1, sizeof(keyed_edge));
+        int64_t m1 = 0;
+        for (int64_t e = 0; e < me; e++)
+            if (hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ) ord[m1++] = ke[e];
+        int64_t q = m1;
+        for (int64_t e = 0; e < me; e++)
+            if (!(hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ)) ord[q++] = ke[e];
+        qsort(ord + m1, (size_t)(me - m1), sizeof(keyed_edge), cmp_plain_key);
+        memcpy(ke, ord, (size_t)me * sizeof(keyed_edge));
+        free(ord);
+        free(tnz);
+    }
 
     ref_lp* lp = (ref_lp*)calloc(1, sizeof(ref_lp));
     lp->problem = problem;
@@ -362,14 +391,16 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     }
     free(ke);
 
-    /* incident edges of each vertex in ascending edge (= row) order */
+    /* incident edges of each vertex (R-17): the rows where it is the larger
+     * endpoint in ascending row order, then the rows where it is the smaller one */
     int64_t* iptr = (int64_t*)xcalloc(n + 1, sizeof(int64_t));
     for (int64_t e = 0; e < me; e++) { iptr[lp->eu[e] + 1]++; iptr[lp->ev[e] + 1]++; }
     for (int64_t v = 0; v < n; v++) iptr[v + 1] += iptr[v];
     int64_t* ifill = (int64_t*)xcalloc(n + 1, sizeof(int64_t));
     int64_t* inc = (int64_t*)xcalloc(2 * me, sizeof(int64_t));
     for (int64_t v = 0; v < n; v++) ifill[v] = iptr[v];
-    for (int64_t e = 0; e < me; e++) { inc[ifill[lp->eu[e]]++] = e; inc[ifill[lp->ev[e]]++] = e; }
+    for (int64_t e = 0; e < me; e++) inc[ifill[lp->ev[e]]++] = e;
+    for (int64_t e = 0; e < me; e++) inc[ifill[lp->eu[e]]++] = e;
     free(ifill);
 
     if (problem == PROB_VC || problem == PROB_MIS) {

@@ -30,7 +30,8 @@ enum Flag { FLAG_BAD_INPUT = 0, FLAG_DUP_TERMINAL = 1, FLAG_BAD_CSC = 2, FLAG_BA
 // key(u < v) = ((u >> kRowRangeShift) n + v) 2^kRowRangeShift + (u mod 2^kRowRangeShift):
 // (range of u, v, u) in 2 log2(n) bits; invalid pairs and self-loops take `sent`
 // (> every key) and sort last
-__global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* __restrict__ src,
+// ranged = false (MWC): key = v n + u, (v, u) order
+__global__ void k_make_keys(int64_t E, int64_t n, bool ranged, uint64_t sent, const int32_t* __restrict__ src,
                             const int32_t* __restrict__ dst, uint64_t* __restrict__ keys,
                             int32_t* __restrict__ idx, int32_t* flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
@@ -42,20 +43,50 @@ __global__ void k_make_keys(int64_t E, int64_t n, uint64_t sent, const int32_t* 
             keys[i] = sent; // self-loop: sorts last, dropped
         } else {
             uint64_t a = (uint64_t)(u < v ? u : v), b = (uint64_t)(u < v ? v : u);
-            keys[i] = ((((a >> kRowRangeShift) * (uint64_t)n + b)) << kRowRangeShift) | (a & (kRowRange - 1));
+            keys[i] = ranged ? ((((a >> kRowRangeShift) * (uint64_t)n + b)) << kRowRangeShift) | (a & (kRowRange - 1))
+                             : b * (uint64_t)n + a;
         }
         if (idx) idx[i] = (int32_t)i;
     }
 }
 
-__global__ void k_decode_edges(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
+__global__ void k_decode_edges(int64_t m, int64_t n, bool ranged, const uint64_t* __restrict__ keys,
+                               int2* __restrict__ edges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
+        if (!ranged) {
+            edges[e] = make_int2((int32_t)(k % (uint64_t)n), (int32_t)(k / (uint64_t)n));
+            continue;
+        }
         const uint64_t gv = k >> kRowRangeShift;    // g n + max
         const uint64_t g = gv / (uint64_t)n;
         edges[e] = make_int2((int32_t)((g << kRowRangeShift) | (k & (kRowRange - 1))), (int32_t)(gv - g * (uint64_t)n));
     }
 }
+// R-17 hub partition (VC / MIS): incidences per tile of 32 vertices
+__global__ void k_tile_counts(int64_t m, const int2* __restrict__ edges, int32_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 - lane < m;
+         e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int2 uv = e0 < m ? edges[e0] : make_int2(-32, -32);
+        const int tu = uv.x >> 5, tv = uv.y >> 5;
+        unsigned same = __match_any_sync(0xffffffffu, tv);
+        if (tv >= 0 && lane == __ffs(same) - 1) atomicAdd(cnt + tv, __popc(same));
+        same = __match_any_sync(0xffffffffu, tu);
+        if (tu >= 0 && lane == __ffs(same) - 1) atomicAdd(cnt + tu, __popc(same));
+    }
+}
+struct HubMaxRow {  // the row's max endpoint lies in a hub tile; row = (min, max) as uint64
+    const int32_t* cnt;
+    __device__ __forceinline__ bool operator()(uint64_t row) const { return cnt[(int32_t)(row >> 32) >> 5] > kHeavy; }
+};
+__global__ void k_plain_keys(int64_t m, int64_t n, const int2* __restrict__ rows, uint64_t* __restrict__ keys) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int2 uv = rows[e];
+        keys[e] = (uint64_t)uv.y * (uint64_t)n + (uint64_t)uv.x;
+    }
+}
+
 // (endpoint, e) pairs for the stable by-endpoint sorts (side 0: min, 1: max)
 __global__ void k_vkeys(int64_t m, const int2* __restrict__ edges, int side, int32_t* __restrict__ vkey,
                         int32_t* __restrict__ eval) {
@@ -388,6 +419,10 @@ size_t cub_bytes_graph(int64_t n, int64_t E, bool pairs) {
         cub::DeviceSelect::Unique(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, E);
     mx = b > mx ? b : mx;
     b = 0;
+    cub::DevicePartition::If(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, E,
+                             HubMaxRow{nullptr});
+    mx = b > mx ? b : mx;
+    b = 0;
     cub::DoubleBuffer<int32_t> dv(nullptr, nullptr), de(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, b, dv, de, E, 0, 32);
     mx = b > mx ? b : mx;
@@ -621,8 +656,10 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     if (!graph_keys_fit(n))
         return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "n = %lld: row keys exceed 64 bits", (long long)n);
     if (E > 0) {
-        const uint64_t sent = graph_key_sentinel(n);
-        k_make_keys<<<grid_for(E, T), T, 0, s>>>(E, n, sent, srcd, dstd, t.keys, mwc ? t.idx : nullptr, lp->flags);
+        const bool ranged = !mwc;
+        const uint64_t sent = ranged ? graph_key_sentinel(n) : (uint64_t)n * (uint64_t)n;
+        k_make_keys<<<grid_for(E, T), T, 0, s>>>(E, n, ranged, sent, srcd, dstd, t.keys, mwc ? t.idx : nullptr,
+                                                 lp->flags);
         const int end_bit = bits_for(sent);
         size_t cb = t.cub_bytes;
         cub::DoubleBuffer<uint64_t> dk(t.keys, t.keys2);
@@ -654,10 +691,35 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
         int64_t rows = mwc ? 2 * (int64_t)k * m : m;
         if (rows >= ((int64_t)1 << 31))
             return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "too many rows (%lld) for int32 row indices", (long long)rows);
-        if (m > 0) k_decode_edges<<<grid_for(m, T), T, 0, s>>>(m, n, uniq, (int2*)d.edges);
+        if (m > 0) k_decode_edges<<<grid_for(m, T), T, 0, s>>>(m, n, ranged, uniq, (int2*)d.edges);
         if (mwc && m > 0) k_gather_ew<<<grid_for(m, T), T, 0, s>>>(m, first_idx, t.ew_in, (float*)d.ew);
     }
     d.m_edges = m;
+    d.m_hub_rows = 0;
+    if (!mwc && m > 0) {
+        // ---- R-17 hub partition: rows with a hub max endpoint keep the ranged order,
+        // the others follow in (max, min) order
+        int32_t* tcnt = t.us;  // n_tiles <= n counters, rewritten below
+        const int64_t n_tiles = (n + 31) / 32;
+        CUDA_TRY(lp, cudaMemsetAsync(tcnt, 0, (size_t)n_tiles * 4, s));
+        k_tile_counts<<<grid_for(m, T), T, 0, s>>>(m, d.edges, tcnt);
+        size_t cb = t.cub_bytes;
+        uint64_t* part = t.keys;
+        CUDA_TRY(lp, cub::DevicePartition::If(t.cub, cb, (const uint64_t*)d.edges, part, t.nsel, m, HubMaxRow{tcnt}, s));
+        int64_t m1 = 0;
+        CUDA_TRY(lp, cudaMemcpyAsync(&m1, t.nsel, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        d.m_hub_rows = m1;
+        const int64_t m2 = m - m1;
+        if (m1 > 0) CUDA_TRY(lp, cudaMemcpyAsync((void*)d.edges, part, (size_t)m1 * 8, cudaMemcpyDeviceToDevice, s));
+        if (m2 > 0) {
+            k_plain_keys<<<grid_for(m2, T), T, 0, s>>>(m2, n, (const int2*)(part + m1), t.keys2);
+            cub::DoubleBuffer<uint64_t> dk(t.keys2, t.keys);
+            cb = t.cub_bytes;
+            CUDA_TRY(lp, cub::DeviceRadixSort::SortKeys(t.cub, cb, dk, m2, 0, bits_for((uint64_t)n * (uint64_t)n), s));
+            k_decode_edges<<<grid_for(m2, T), T, 0, s>>>(m2, n, false, dk.Current(), (int2*)d.edges + m1);
+        }
+    }
     THETIS_TRY(check_cuda(lp, "build: keys"));
 
     // ---- incidence lists, ascending row order per vertex

@@ -33,7 +33,6 @@ namespace thetis {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int64_t kHeavy = 512;     // async: a tile whose scalar columns hold more nonzeros is a hub tile (R-6)
 constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the warp path
 
 struct StepParams {
@@ -477,7 +476,7 @@ __global__ void k_hub_ids(int64_t n_heavy, const int32_t* heavy_tiles, int32_t* 
 // first row of every range of min endpoints (rows are sorted by range): lower bound
 __global__ void k_range_starts(DevLP L, int64_t n_ranges, int32_t* start) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= n_ranges; g += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = 0, hi = L.m;
+        int64_t lo = 0, hi = L.m_hub_rows;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
             if ((int64_t)(L.edges[mid].x >> kRowRangeShift) < g) lo = mid + 1;
@@ -522,7 +521,7 @@ __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range
         const int2 uv = L.edges[e];
         const int32_t g = uv.x >> kRowRangeShift;
         int32_t su = hub_slot(H, uv.x);
-        if (su >= 0 && range_shared[g]) su = uv.x - (g << kRowRangeShift);
+        if (su >= 0 && e < L.m_hub_rows && range_shared[g]) su = uv.x - (g << kRowRangeShift);
         pk[e] = make_int2(su, hub_slot(H, uv.y));
     }
 }
@@ -888,7 +887,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         H.next = C.take<unsigned long long>(32 * 2);
         const int64_t n_ranges = (L.n_scalar + kRowRange - 1) / kRowRange;
         int32_t* rstart = C.take<int32_t>(n_ranges + 1);
-        const int64_t max_items = L.m / kItemRows + 2 * n_ranges + 2;
+        const int64_t max_items = 2 * (L.m / kItemRows) + 2 * n_ranges + 4;
         int4* items = C.take<int4>(H.n_heavy > 0 ? max_items : 1);
         H.items = items;
         uint8_t* range_shared = C.take<uint8_t>(n_ranges + 1);
@@ -920,6 +919,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                     it.push_back(make_int4((int)g, b0, b1, 0));
                 }
             }
+            // rows with a light max endpoint (R-17: after the ranged part): global items
+            for (int64_t p = L.m_hub_rows; p < L.m; p += kItemRows)
+                it.push_back(make_int4(0, (int)p, (int)(p + kItemRows < L.m ? p + kItemRows : L.m), 0));
             if ((int64_t)it.size() > max_items) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "row pass items");
             H.n_items = (int)it.size();
             if (!it.empty())

@@ -14,6 +14,7 @@ namespace thetis {
 constexpr int kTile = 32;          // units per async tile (R-6)
 constexpr int kRowRangeShift = 14; // graph LP rows grouped by min endpoint >> 14 (R-17)
 constexpr int kRowRange = 1 << kRowRangeShift;
+constexpr int64_t kHeavy = 512;    // a tile whose scalar columns hold more nonzeros is a hub tile (R-6, R-17)
 constexpr int kMaxK = 32;          // max simplex block size
 constexpr uint32_t kSignBit = 0x80000000u;
 constexpr uint32_t kRowMask = 0x7FFFFFFFu;
@@ -27,6 +28,7 @@ constexpr int kRedThreads = 256;
 struct DevLP {
     int problem, obj_sense, k;
     int64_t m, n_s, n_ineq, N, nnz_s, U, n_blocks, n_scalar, n_vert, m_edges;
+    int64_t m_hub_rows;        // VC / MIS: rows [0, m_hub_rows) have a hub max endpoint (R-17)
     // A, structural part: CSC, rows ascending.  val == nullptr: coefficient
     // +1, or -1 when bit 31 of rowidx is set.
     const int64_t* colptr;

@@ -17,6 +17,29 @@ def unique_edges(n, src, dst):
     return sorted(s)
 
 
+def row_order(n, edges, hubs=True, hub_nnz=512):
+    """R-17 written out: rows whose larger endpoint lies in a hub tile (32 consecutive
+    vertex ids with more than hub_nnz incidences; VC / MIS only) in (u >> 14, v, u)
+    order, then the other rows in (v, u) order."""
+    tnz = {}
+    for u, v in edges:
+        tnz[u >> 5] = tnz.get(u >> 5, 0) + 1
+        tnz[v >> 5] = tnz.get(v >> 5, 0) + 1
+    hub = [e for e in edges if hubs and tnz[e[1] >> 5] > hub_nnz]
+    rest = [e for e in edges if not (hubs and tnz[e[1] >> 5] > hub_nnz)]
+    return sorted(hub, key=lambda e: (e[0] >> 14, e[1], e[0])) + sorted(rest, key=lambda e: (e[1], e[0]))
+
+
+def incidence(n, rows):
+    """per vertex: the rows where it is the larger endpoint, then the smaller (R-17)"""
+    inc = [[] for _ in range(n)]
+    for i, (u, v) in enumerate(rows):
+        inc[v].append(i)
+    for i, (u, v) in enumerate(rows):
+        inc[u].append(i)
+    return inc
+
+
 def _grid_points(n, values):
     vals = np.array(values, dtype=np.float64)
     idx = np.indices((len(vals),) * n).reshape(n, -1).T

@@ -258,23 +258,40 @@ def test_maintained_residual_equals_recomputed():
         assert lp.objective(10.0)["drift_inf"] < 1e-12
 
 
-def test_graph_row_order_spans_ranges():
-    # R-17: rows sorted by (min >> 14, max, min); ids spread over four 2^14 ranges so the
-    # grouping by the min endpoint's range differs from a plain (max, min) order.  Each
-    # column lists its rows in ascending row order.
+def hub_graph(n, m, seed):
+    # random edges over four 2^14 ranges plus two hub tiles (ids 0-31 and 20000-20031)
+    # with > 512 incidences each
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m)
+    dst = rng.integers(0, n, m)
+    hs = np.concatenate([rng.integers(0, 32, 700), rng.integers(20000, 20032, 700)])
+    hd = rng.integers(0, n, 1400)
+    return (np.concatenate([src, hs]).astype(np.int32), np.concatenate([dst, hd]).astype(np.int32))
+
+
+@pytest.mark.parametrize("problem", [VC, MIS, MWC])
+def test_graph_row_order_and_incidence(problem):
+    # R-17: hub-partitioned row order; every column lists its max-endpoint rows, then its
+    # min-endpoint rows, each ascending (checked against the plain definition)
     n = 4 << 14
-    src, dst = small_graph(n, 3000, 21)
+    src, dst = hub_graph(n, 3000, 21)
     edges = bf.unique_edges(n, src, dst)
-    lp = RefLP.graph(VC, n, src, dst, vertex_w=np.ones(n, np.float32))
+    if problem == MWC:
+        lp = RefLP.graph(MWC, n, src, dst, edge_w=np.ones(len(src), np.float32), k=2,
+                         terminals=[1, 2], t_per_label=1)
+    else:
+        lp = RefLP.graph(problem, n, src, dst, vertex_w=np.ones(n, np.float32))
     eu, ev = lp.edges()
-    want = sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
-    assert want != sorted(edges, key=lambda e: (e[1], e[0]))
+    want = bf.row_order(n, edges, hubs=problem != MWC)
+    if problem != MWC:
+        assert want != sorted(edges, key=lambda e: (e[1], e[0]))  # the hub part is non-empty
+        assert want != sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
     assert list(zip(eu.tolist(), ev.tolist())) == want
-    colptr, rowidx, _ = lp.csc()
-    for v in range(0, n, 97):
-        rows = rowidx[colptr[v]:colptr[v + 1]]
-        assert (np.diff(rows) > 0).all()
-        assert sorted(rows.tolist()) == [i for i, (a, b) in enumerate(want) if v in (a, b)]
+    if problem != MWC:
+        colptr, rowidx, _ = lp.csc()
+        inc = bf.incidence(n, want)
+        for v in list(range(0, 64)) + list(range(19990, 20040)) + list(range(0, n, 97)):
+            assert rowidx[colptr[v]:colptr[v + 1]].tolist() == inc[v]
 
 
 def test_graph_encoding_counts():
@@ -286,7 +303,7 @@ def test_graph_encoding_counts():
     lp = RefLP.graph(VC, 30, src, dst, vertex_w=w)
     assert lp.m == len(edges) and lp.nnz_struct == 2 * len(edges) and lp.n_ineq == len(edges)
     eu, ev = lp.edges()
-    assert list(zip(eu.tolist(), ev.tolist())) == sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
+    assert list(zip(eu.tolist(), ev.tolist())) == bf.row_order(30, edges)
     b, sense, c = lp.rows()
     assert (b == 1).all() and (sense == oracle.SENSE_GE).all()
     lpm = RefLP.graph(MIS, 30, src, dst, vertex_w=w)
