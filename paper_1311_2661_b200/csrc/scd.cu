@@ -487,7 +487,7 @@ __global__ void k_range_starts(DevLP L, int64_t n_ranges, int32_t* start) {
 }
 
 constexpr int kPassThreads = 1024;             // one block per SM, shared d / D of one range
-constexpr int64_t kItemRows = 1 << 17;         // rows per work item
+constexpr int64_t kItemRows = 1 << 19;         // rows per work item
 constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side through global memory
 
 // v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
@@ -576,9 +576,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             for (int t = threadIdx.x; t < kRowRange / 32; t += blockDim.x)
                 s_hub[t] = (int64_t)base + t * 32 < L.n_scalar ? H.hub_id[(base >> 5) + t] : -1;
             __syncthreads();
-            for (int i = threadIdx.x; i < kRowRange; i += blockDim.x) {
+            constexpr int kPer = kRowRange / kPassThreads;
+            float pv[kPer];
+#pragma unroll
+            for (int q = 0; q < kPer; q++) {  // all loads in flight together
+                const int i = threadIdx.x + q * kPassThreads;
                 const int32_t h = s_hub[i >> 5];
-                s_pend[i] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
+                pv[q] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < kPer; q++) {
+                const int i = threadIdx.x + q * kPassThreads;
+                s_pend[i] = pv[q];
                 s_lo[i] = 0u;
                 s_hi[i] = 0;
             }
