@@ -125,8 +125,14 @@ THETIS_API int thetis_build_graph_lp_workspace(int problem, int64_t n, int64_t n
  *  src, dst   int32[n_edges] endpoints in [0, n); orientation free; self-loops
  *             dropped; duplicate pairs kept once (the first occurrence's
  *             edge weight is used).  Rows follow the unique canonical pairs
- *             (u < v) in (v, u) order (a vertex's edges to smaller ids are one
- *             contiguous run of rows).
+ *             (u < v) (R-17): VC / MIS rows whose larger endpoint v
+ *             lies in a hub tile (32 consecutive ids with > 512 incidences)
+ *             first, sorted by (u >> 14, v, u); then the other rows (all MWC
+ *             rows) sorted by (v, u).  Each CSC column lists the rows where the
+ *             vertex is the larger endpoint, then those where it is the smaller,
+ *             each in ascending row order.  n must satisfy
+ *             ((n-2) >> 14) * n * 2^14 + ... < 2^64 (n <= 2^32), else
+ *             THETIS_ERR_NOT_SUPPORTED.
  *  vertex_w   float[n]: VC costs c_v (min) / MIS weights w_v (max).
  *  edge_w     float[n_edges]: MWC edge costs c_uv (objective 1/2 sum c_uv sum_l x_uv^l).
  *  k          MWC labels (2..32); terminals int32[k * t_per_label], label-major
