@@ -241,6 +241,22 @@ def run_thetis(args):
     nnz_step = last["st"].nnz_processed
     value = job_throughput(upd_step, args.steps, ws_n, ms)
     ep_med = statistics.median(epoch_ms)
+    # live per-kernel device time of the epoch's launches (CUDA events on the solve stream)
+    kst = [r["st"] for r in recs]
+    n_rp = sum(x.row_pass_launches for x in kst)
+    n_ep = sum(min(int(x.epochs), 64) for x in kst)
+    kernels = None
+    if n_rp:
+        kernels = {
+            "k_rows_pass": {"ms_per_launch": sum(x.ms_row_pass for x in kst) / n_rp,
+                            "launches_per_step": n_rp / len(kst)},
+            "k_hub_update": {"ms_per_launch": sum(x.ms_hub_update for x in kst) / n_ep,
+                             "launches_per_step": n_ep / len(kst)},
+            "k_async": {"ms_per_launch": sum(x.ms_tiles for x in kst) / n_ep, "launches_per_step": n_ep / len(kst)},
+        }
+        tot = sum(v["ms_per_launch"] * v["launches_per_step"] for v in kernels.values())
+        for v in kernels.values():
+            v["share_of_epochs"] = v["ms_per_launch"] * v["launches_per_step"] / tot
     b_epoch = algorithmic_bytes(dims.n_struct, dims.nnz_struct, dims.m)
     peak, peak_src = load_peaks()
     achieved = b_epoch / (ep_med / 1e3) / 1e9
@@ -310,8 +326,9 @@ def run_thetis(args):
                   "GBps": achieved, "frac_of_8TBps_nominal": achieved / 8000.0},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(),
-                     "kernel": "one SCD epoch = k_hub_rows_gather + k_hub_update + k_rows_hub_slack + k_async "
-                               "(CUDA events around each epoch on the launching stream)", "peak_source": peak_src},
+                     "kernel": "one SCD epoch = k_rows_pass + k_hub_update + k_async (CUDA events around each "
+                               "epoch on the launching stream; SURVEY 8(d) bytes per epoch)", "peak_source": peak_src,
+                     "kernels": kernels},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),
                    "selected": int(rr.n_selected)},

@@ -45,7 +45,9 @@ class SolveStats(ctypes.Structure):
     _fields_ = [("epochs", ctypes.c_int64), ("coordinate_updates", ctypes.c_int64),
                 ("nnz_processed", ctypes.c_int64), ("ms_total", ctypes.c_double),
                 ("ms_per_epoch", ctypes.c_float * THETIS_MAX_EPOCH_TIMES), ("L_max", ctypes.c_double),
-                ("n_colours", ctypes.c_int64), ("mode", ctypes.c_int32), ("step_rule", ctypes.c_int32)]
+                ("n_colours", ctypes.c_int64), ("mode", ctypes.c_int32), ("step_rule", ctypes.c_int32),
+                ("ms_row_pass", ctypes.c_double), ("ms_hub_update", ctypes.c_double),
+                ("ms_tiles", ctypes.c_double), ("row_pass_launches", ctypes.c_int64)]
 
 
 class Objective(ctypes.Structure):

@@ -65,6 +65,7 @@ void destroy(thetis_lp* lp) {
     if (lp->ev_fork) cudaEventDestroy(lp->ev_fork);
     if (lp->ev_join) cudaEventDestroy(lp->ev_join);
     for (auto e : lp->ev_epoch) cudaEventDestroy(e);
+    for (auto e : lp->ev_kern) cudaEventDestroy(e);
     delete lp;
 }
 

@@ -951,6 +951,17 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             for (auto& e : lp->ev_epoch) CUDA_TRY(lp, cudaEventCreate(&e));
         }
     }
+    const int n_timed = epochs < THETIS_MAX_EPOCH_TIMES ? epochs : THETIS_MAX_EPOCH_TIMES;
+    if (timed && lp->ev_kern.empty()) {
+        lp->ev_kern.resize(3 * THETIS_MAX_EPOCH_TIMES);
+        for (auto& e : lp->ev_kern) CUDA_TRY(lp, cudaEventCreate(&e));
+    }
+    // per timed epoch e: [3e] after the row pass, [3e+1] after the hub update, [3e+2]
+    // after the tiles (before the final application of the pending steps)
+    auto kern_mark = [&](int e, int k) -> int {
+        if (timed && e < n_timed) CUDA_TRY(lp, cudaEventRecord(lp->ev_kern[3 * e + k], s));
+        return THETIS_OK;
+    };
     cudaEvent_t ev_start = timed ? lp->ev_epoch[0] : nullptr;
     if (timed) CUDA_TRY(lp, cudaEventRecord(ev_start, s));
     for (int e = 0; e < epochs; e++) {
@@ -967,7 +978,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
                 if (anchored) k_rows_pass<true, true><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0, 0);
                 else k_rows_pass<true, false><<<(unsigned)hub_blocks, kPassThreads, kPassSmem, s>>>(L, P, H, e > 0, g_exp);
+                THETIS_TRY(kern_mark(e, 0));
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
+                THETIS_TRY(kern_mark(e, 1));
             } else if (L.n_ineq > 0) {
                 k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
             }
@@ -978,6 +991,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
         }
+        if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) THETIS_TRY(kern_mark(e, 2));
         // the last epoch's hub steps are still pending: apply them, r = A z - b again
         if (e == epochs - 1 && mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
@@ -1000,6 +1014,22 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             CUDA_TRY(lp, cudaEventElapsedTime(&ms, lp->ev_epoch[e], lp->ev_epoch[e + 1]));
             st->ms_per_epoch[e] = ms;
             st->ms_total += ms;
+            if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
+                float a = 0, b = 0, c = 0;
+                CUDA_TRY(lp, cudaEventElapsedTime(&a, lp->ev_epoch[e], lp->ev_kern[3 * e]));
+                CUDA_TRY(lp, cudaEventElapsedTime(&b, lp->ev_kern[3 * e], lp->ev_kern[3 * e + 1]));
+                CUDA_TRY(lp, cudaEventElapsedTime(&c, lp->ev_kern[3 * e + 1], lp->ev_kern[3 * e + 2]));
+                st->ms_row_pass += a;
+                st->ms_hub_update += b;
+                st->ms_tiles += c;
+                st->row_pass_launches += 1;
+                if (e == epochs - 1) {  // the final application of the pending steps
+                    float f = 0;
+                    CUDA_TRY(lp, cudaEventElapsedTime(&f, lp->ev_kern[3 * e + 2], lp->ev_epoch[e + 1]));
+                    st->ms_row_pass += f;
+                    st->row_pass_launches += 1;
+                }
+            }
         }
     }
     return THETIS_OK;

@@ -173,6 +173,7 @@ struct thetis_lp {
     cudaStream_t side = nullptr;   // second stream: hub-hub row pass beside the light tiles
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_epoch;
+    std::vector<cudaEvent_t> ev_kern;   // per-kernel marks of timed async epochs
     char* ws = nullptr;
     size_t ws_bytes = 0;
     // regions inside ws

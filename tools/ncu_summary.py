@@ -65,17 +65,19 @@ def main(tag, out_dir):
     lines = [f"# {tag}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
              "lts__t_sector_hit_rate.pct on the epoch kernels of one bench step (20 epochs)",
              f"{'launches':>8} {'GB read':>9} {'GB write':>9} {'ms':>8} {'L2 hit%':>8}  kernel (per launch)"]
-    epoch_bytes = 0.0
-    n_epochs = None
+    epoch_total = 0.0
+    # one k_async (or k_slack_sweep) launch per epoch; kernels launched once per call (the
+    # application of the pending hub steps) are spread over the call's epochs
+    n_epochs = max([agg[k]["launches"] for k in agg if k.startswith(("k_async", "k_slack"))] or [1])
     for nm, c in sorted(agg.items()):
         n = c["launches"]
         rd, wr = c["dram__bytes_read.sum"] / n, c["dram__bytes_write.sum"] / n
         lines.append(f"{n:8d} {rd / 1e9:9.3f} {wr / 1e9:9.3f} {c['gpu__time_duration.sum'] / n / 1e6:8.3f} "
                      f"{c['hit'] / n:8.1f}  {nm}")
-        if nm.startswith(("k_async", "k_hub", "k_rows", "k_slack")):
-            epoch_bytes += rd + wr
-            n_epochs = n if n_epochs is None else max(n_epochs, n)
-    lines.append(f"# DRAM bytes per epoch (sum over the epoch's kernels): {epoch_bytes / 1e9:.3f} GB")
+        if nm.startswith(("k_async", "k_hub_update", "k_rows", "k_slack")):
+            epoch_total += c["dram__bytes_read.sum"] + c["dram__bytes_write.sum"]
+    epoch_bytes = epoch_total / n_epochs
+    lines.append(f"# DRAM bytes per epoch (epoch kernels' bytes over {n_epochs} epochs): {epoch_bytes / 1e9:.3f} GB")
     open(os.path.join(out_dir, f"{tag}_epoch_dram.txt"), "w").write("\n".join(lines) + "\n")
     json.dump({"round": tag, "epoch_dram_bytes": epoch_bytes,
                "note": "sum of dram__bytes_read.sum + dram__bytes_write.sum over the kernels of one SCD epoch"},
