@@ -563,6 +563,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
     float* __restrict__ r = L.r;
     float* __restrict__ zs = L.z + L.n_s;
     const int2* __restrict__ pk = H.pk;
+    const bool zvec = (L.n_s & 3) == 0;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) s_it = (int)atomicAdd(H.next, 1ull);
@@ -576,48 +577,77 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             for (int t = threadIdx.x; t < kRowRange / 32; t += blockDim.x)
                 s_hub[t] = (int64_t)base + t * 32 < L.n_scalar ? H.hub_id[(base >> 5) + t] : -1;
             __syncthreads();
-            constexpr int kPer = kRowRange / kPassThreads;
+            constexpr int kPer = (kRowRange + kPassThreads - 1) / kPassThreads;
             float pv[kPer];
 #pragma unroll
             for (int q = 0; q < kPer; q++) {  // all loads in flight together
                 const int i = threadIdx.x + q * kPassThreads;
-                const int32_t h = s_hub[i >> 5];
+                const int32_t h = i < kRowRange ? s_hub[i >> 5] : -1;
                 pv[q] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
             }
 #pragma unroll
             for (int q = 0; q < kPer; q++) {
                 const int i = threadIdx.x + q * kPassThreads;
-                s_pend[i] = pv[q];
-                s_lo[i] = 0u;
-                s_hi[i] = 0;
+                if (i < kRowRange) {
+                    s_pend[i] = pv[q];
+                    s_lo[i] = 0u;
+                    s_hi[i] = 0;
+                }
             }
             __syncthreads();
         }
-        for (int64_t e0 = w.y + threadIdx.x; e0 - lane < w.z; e0 += kPassRows * (int64_t)blockDim.x) {
-            int2 key[kPassRows];
-            float r0[kPassRows], z[kPassRows];
+        // four consecutive rows per thread (vector loads; the max side merges its runs in
+        // the thread first, then across the warp), groups 4-aligned from a0
+        const int64_t a0 = w.y & ~(int64_t)3;
+        for (int64_t g0 = a0 + 4 * (int64_t)threadIdx.x; g0 - 4 * lane < w.z; g0 += 4 * (int64_t)blockDim.x) {
+            int2 key[4];
+            float r0[4], z[4];
+            bool ok[4];
+            if (g0 + 4 <= L.m && g0 >= w.y && g0 + 4 <= w.z) {
+                const int4 k01 = __ldcs((const int4*)(pk + g0)), k23 = __ldcs((const int4*)(pk + g0 + 2));
+                key[0] = make_int2(k01.x, k01.y); key[1] = make_int2(k01.z, k01.w);
+                key[2] = make_int2(k23.x, k23.y); key[3] = make_int2(k23.z, k23.w);
+                const float4 rr = __ldcs((const float4*)(r + g0));
+                r0[0] = rr.x; r0[1] = rr.y; r0[2] = rr.z; r0[3] = rr.w;
+                if (kSlack) {
+                    if (zvec) {
+                        const float4 zz = __ldcs((const float4*)(zs + g0));
+                        z[0] = zz.x; z[1] = zz.y; z[2] = zz.z; z[3] = zz.w;
+                    } else {
 #pragma unroll
-            for (int q = 0; q < kPassRows; q++) {
-                const int64_t e = e0 + q * (int64_t)blockDim.x;
-                const bool take = e < w.z;
-                key[q] = take ? __ldcs(pk + e) : make_int2(-1, -1);
-                r0[q] = take ? __ldcs(r + e) : 0.0f;
-                if (kSlack) z[q] = take ? __ldcs(zs + e) : 0.0f;
+                        for (int j = 0; j < 4; j++) z[j] = __ldcs(zs + g0 + j);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++) ok[j] = true;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int64_t e = g0 + j;
+                    ok[j] = e >= w.y && e < w.z;
+                    key[j] = ok[j] ? __ldcs(pk + e) : make_int2(-1, -1);
+                    r0[j] = ok[j] ? __ldcs(r + e) : 0.0f;
+                    z[j] = kSlack && ok[j] ? __ldcs(zs + e) : 0.0f;
+                }
             }
-            float rv[kPassRows];
+            float rv[4];
+            float dvp = 0.0f;
 #pragma unroll
-            for (int q = 0; q < kPassRows; q++) {
-                const int64_t e = e0 + q * (int64_t)blockDim.x;
-                const bool take = e < w.z;
+            for (int j = 0; j < 4; j++) {
                 float du = 0.0f, dv = 0.0f;
                 if (apply) {
-                    if (key[q].x >= 0) du = sh ? s_pend[key[q].x] : pend_of(H.hv, key[q].x);
-                    if (key[q].y >= 0 && !(exp & 4)) dv = pend_of(H.hv, key[q].y);
+                    if (key[j].x >= 0) du = sh ? s_pend[key[j].x] : pend_of(H.hv, key[j].x);
+                    if (key[j].y >= 0 && !(exp & 4)) {
+                        // the thread's rows are sorted by max endpoint: reuse the previous load
+                        dv = (j > 0 && key[j].y == key[j - 1].y) ? dvp : pend_of(H.hv, key[j].y);
+                        dvp = dv;
+                    }
                 }
                 const float delta = __fadd_rn(du, dv);
-                float x = delta != 0.0f ? __fadd_rn(r0[q], delta) : r0[q];
-                if (kSlack && take) {
+                float x = delta != 0.0f ? __fadd_rn(r0[j], delta) : r0[j];
+                if (kSlack && ok[j]) {
                     // slack_new<true>: D = sigma r, g = -ua + beta D + (z - zbar) / beta
+                    const int64_t e = g0 + j;
                     float ua = 0.0f, zb = 0.0f;
                     if (kAnchor) {
                         if (L.ubar) ua = __fadd_rn(0.0f, sg < 0.0f ? -L.ubar[e] : L.ubar[e]);
@@ -626,26 +656,59 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                     const float D = __fadd_rn(0.0f, sg < 0.0f ? -x : x);
                     float g = __fsub_rn(0.0f, ua);
                     g = __fadd_rn(g, __fmul_rn(beta, D));
-                    g = __fadd_rn(g, __fmul_rn(__fsub_rn(z[q], zb), inv_beta));
-                    float t = __fsub_rn(z[q], __fmul_rn(g, invLs));
+                    g = __fadd_rn(g, __fmul_rn(__fsub_rn(z[j], zb), inv_beta));
+                    float t = __fsub_rn(z[j], __fmul_rn(g, invLs));
                     t = t < 0.0f ? 0.0f : t;
-                    const float d = __fsub_rn(t, z[q]);
+                    const float d = __fsub_rn(t, z[j]);
                     if (d != 0.0f) {
                         x = __fadd_rn(x, sg < 0.0f ? -d : d);
                         __stcs(zs + e, t);
                     }
                 }
-                if (take && x != r0[q]) __stcs(r + e, x);
-                rv[q] = x;
+                rv[j] = x;
+            }
+            if (ok[0] && ok[1] && ok[2] && ok[3]) {
+                __stcs((float4*)(r + g0), make_float4(rv[0], rv[1], rv[2], rv[3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (ok[j] && rv[j] != r0[j]) __stcs(r + g0 + j, rv[j]);
             }
             if (kSlack) {
 #pragma unroll
-                for (int q = 0; q < kPassRows; q++) {
-                    if (key[q].x >= 0 && !(exp & 2)) {
-                        if (sh) fix_add(s_lo, s_hi, key[q].x, rv[q]);
-                        else atomicAdd(acc_of(H.hv, key[q].x), rv[q]);
+                for (int j = 0; j < 4; j++) {
+                    if (key[j].x >= 0 && !(exp & 2)) {
+                        if (sh) fix_add(s_lo, s_hi, key[j].x, rv[j]);
+                        else atomicAdd(acc_of(H.hv, key[j].x), rv[j]);
                     }
-                    if (!(exp & 1)) add_max_side((float*)H.hv, key[q].y >= 0 ? 2 * key[q].y : -1, rv[q], lane, exp & 8);
+                }
+                if (!(exp & 1)) {
+                    // max side: runs inside the thread; the first run may continue the
+                    // previous lane's last run, the last run may continue into the next lane
+                    const int k0 = key[0].y, k1 = key[1].y, k2 = key[2].y, k3 = key[3].y;
+                    const bool b1 = k1 != k0, b2 = k2 != k1, b3 = k3 != k2;  // run heads at 1, 2, 3
+                    const bool single = !b1 && !b2 && !b3;
+                    float head = rv[0];
+                    if (!b1) head += rv[1];
+                    if (!b1 && !b2) head += rv[2];
+                    if (single) head += rv[3];
+                    float tail = rv[3];
+                    if (!b3) tail += rv[2];
+                    if (!b3 && !b2) tail += rv[1];
+                    if (single) tail = head;
+                    // complete runs strictly inside the thread: {1}, {1, 2} or {2}
+                    if (b1 && b2 && k1 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k1, rv[1]);
+                    if (b1 && !b2 && b3 && k1 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k1, rv[1] + rv[2]);
+                    if (b2 && b3 && k2 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k2, rv[2]);
+                    // a non-single next lane hands its head to my tail when the run continues
+                    const int nk0 = __shfl_down_sync(0xffffffffu, key[0].y, 1);
+                    const float nh = __shfl_down_sync(0xffffffffu, head, 1);
+                    const bool nsingle = __shfl_down_sync(0xffffffffu, (int)single, 1);
+                    if (lane < 31 && !nsingle && nk0 == key[3].y) tail += nh;
+                    const int pk3 = __shfl_up_sync(0xffffffffu, key[3].y, 1);
+                    if (!single && !(lane > 0 && key[0].y == pk3) && key[0].y >= 0)
+                        atomicAdd((float*)H.hv + 2 * (int64_t)key[0].y, head);
+                    add_max_side((float*)H.hv, key[3].y >= 0 ? 2 * key[3].y : -1, tail, lane, exp & 8);
                 }
             }
         }
