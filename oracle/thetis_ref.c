@@ -350,8 +350,9 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
         if (t == 0 || ke[t].key != ke[t - 1].key) ke[me++] = ke[t];
     {
         /* R-17: the rows whose larger endpoint lies in a hub tile (VC / MIS: a tile
-         * of 32 vertices with more than HUB_NNZ incidences) keep this order; the
-         * others follow, sorted by (v, u) */
+         * of 32 vertices with more than HUB_NNZ incidences) keep this order; then the
+         * other rows whose smaller endpoint lies in a hub tile, sorted by (v, u);
+         * then the remaining rows, sorted by (v, u) */
         int64_t n_tiles = (n + 31) / 32;
         int64_t* tnz = (int64_t*)xcalloc(n_tiles + 1, sizeof(int64_t));
         for (int64_t e = 0; e < me; e++) {
@@ -363,10 +364,16 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
         int64_t m1 = 0;
         for (int64_t e = 0; e < me; e++)
             if (hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ) ord[m1++] = ke[e];
-        int64_t q = m1;
+        int64_t m2 = m1;
         for (int64_t e = 0; e < me; e++)
-            if (!(hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ)) ord[q++] = ke[e];
-        qsort(ord + m1, (size_t)(me - m1), sizeof(keyed_edge), cmp_plain_key);
+            if (!(hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ) && hubs && tnz[(ke[e].key & 0xFFFFFFFFu) >> 5] > HUB_NNZ)
+                ord[m2++] = ke[e];
+        int64_t q = m2;
+        for (int64_t e = 0; e < me; e++)
+            if (!(hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ) && !(hubs && tnz[(ke[e].key & 0xFFFFFFFFu) >> 5] > HUB_NNZ))
+                ord[q++] = ke[e];
+        qsort(ord + m1, (size_t)(m2 - m1), sizeof(keyed_edge), cmp_plain_key);
+        qsort(ord + m2, (size_t)(me - m2), sizeof(keyed_edge), cmp_plain_key);
         memcpy(ke, ord, (size_t)me * sizeof(keyed_edge));
         free(ord);
         free(tnz);

@@ -2,10 +2,12 @@
 // LP in HBM (CSC with sign-bit coefficients, unique edge rows, costs, bounds), the
 // initial point z0 with r0 = A z0 - b, and max ||a_j||^2 for L_max (Eq. 7).
 //
-//   rows: one per unique undirected non-loop edge (u < v), ordered by
-//   (u >> kRowRangeShift, v, u) (R-17): the rows whose min endpoint lies in one
-//   range of 2^14 ids are contiguous (the hub step accumulates that side in shared
-//   memory), and within a range a vertex's edges to smaller ids are one run
+//   rows: one per unique undirected non-loop edge (u < v) (R-17).  VC / MIS: first
+//   the rows with a hub max endpoint, ordered by (u >> kRowRangeShift, v, u) (the
+//   rows whose min endpoint lies in one range of 2^14 ids are contiguous: the row
+//   pass accumulates that side in shared memory; within a range a vertex's edges to
+//   smaller ids are one run); then the other rows with a hub min endpoint, then the
+//   rest, each in (v, u) order.  MWC: all rows in (v, u) order
 //   VC  (Eq. 2):   row e = (u < v): x_u + x_v - s_e = 1
 //   MIS (App. B.2):           row e:           x_u + x_v + s_e = 1, max w^T x
 //   MWC (App. B.3): x_v^l at v*k+l, x_e^l at n*k+e*k+l;
@@ -128,10 +130,27 @@ struct HubMaxRow {  // the row's max endpoint lies in a hub tile; row = (min, ma
     const int32_t* cnt;
     __device__ __forceinline__ bool operator()(uint64_t row) const { return cnt[(int32_t)(row >> 32) >> 5] > kHeavy; }
 };
-__global__ void k_plain_keys(int64_t m, int64_t n, const int2* __restrict__ rows, uint64_t* __restrict__ keys) {
+// rows with a light max endpoint (R-17): key = (light(u) n + v) n + u, i.e. the rows
+// with a hub min endpoint first, each part in (v, u) order; counts the first part
+__global__ void k_plain_keys(int64_t m, int64_t n, const int2* __restrict__ rows, const int32_t* __restrict__ cnt,
+                             uint64_t* __restrict__ keys, unsigned long long* n_hub_min) {
+    unsigned long long c = 0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         const int2 uv = rows[e];
-        keys[e] = (uint64_t)uv.y * (uint64_t)n + (uint64_t)uv.x;
+        const bool hub_u = cnt[uv.x >> 5] > kHeavy;
+        c += hub_u;
+        keys[e] = ((hub_u ? 0ull : (uint64_t)n) + (uint64_t)uv.y) * (uint64_t)n + (uint64_t)uv.x;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_hub_min, c);
+}
+// decode (light(u) n + v) n + u
+__global__ void k_decode_plain(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[e];
+        const uint64_t hv = k / (uint64_t)n;
+        edges[e] = make_int2((int32_t)(k - hv * (uint64_t)n), (int32_t)(hv % (uint64_t)n));
     }
 }
 
@@ -549,6 +568,11 @@ static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* 
     t.cub = C.take<char>((int64_t)t.cub_bytes);
     size_t total = C.off;
     size_t post = post_build_temp(S, n_s, n);
+    if (!mwc) {  // the async solve's row pass (scd.cu): row keys, hub slots, light slots, items
+        const size_t asy = 8 * (size_t)E + 16 * ((size_t)n + 32) + 4 * (size_t)((n + 31) / 32) +
+                           16 * (size_t)(2 * (E >> 19) + 2 * ((n >> 14) + 1) + 4) + (size_t)(n >> 14) + (1 << 20);
+        if (asy > post) post = asy;
+    }
     if (temp_start + post > total) total = temp_start + post;
     if (carve) {
         DevLP& d = lp->d;
@@ -747,6 +771,7 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     }
     d.m_edges = m;
     d.m_hub_rows = 0;
+    d.m_defer_rows = 0;
     if (!mwc && m > 0) {
         // ---- R-17 hub partition: rows with a hub max endpoint keep the ranged order,
         // the others follow in (max, min) order
@@ -761,14 +786,21 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
         CUDA_TRY(lp, cudaMemcpyAsync(&m1, t.nsel, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(lp, cudaStreamSynchronize(s));
         d.m_hub_rows = m1;
+        d.m_defer_rows = m1;
         const int64_t m2 = m - m1;
         if (m1 > 0) CUDA_TRY(lp, cudaMemcpyAsync((void*)d.edges, part, (size_t)m1 * 8, cudaMemcpyDeviceToDevice, s));
         if (m2 > 0) {
-            k_plain_keys<<<grid_for(m2, T), T, 0, s>>>(m2, n, (const int2*)(part + m1), t.keys2);
+            CUDA_TRY(lp, cudaMemsetAsync(t.nsel, 0, 8, s));
+            k_plain_keys<<<grid_for(m2, T), T, 0, s>>>(m2, n, (const int2*)(part + m1), tcnt, t.keys2,
+                                                       (unsigned long long*)t.nsel);
             cub::DoubleBuffer<uint64_t> dk(t.keys2, t.keys);
             cb = t.cub_bytes;
-            CUDA_TRY(lp, sort_keys_u64(t.cub, cb, dk, m2, bits_for((uint64_t)n * (uint64_t)n), s));
-            k_decode_edges<<<grid_for(m2, T), T, 0, s>>>(m2, n, false, dk.Current(), (int2*)d.edges + m1);
+            CUDA_TRY(lp, sort_keys_u64(t.cub, cb, dk, m2, bits_for(2 * (uint64_t)n * (uint64_t)n), s));
+            k_decode_plain<<<grid_for(m2, T), T, 0, s>>>(m2, n, dk.Current(), (int2*)d.edges + m1);
+            int64_t ma = 0;
+            CUDA_TRY(lp, cudaMemcpyAsync(&ma, t.nsel, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+            d.m_defer_rows = m1 + ma;
         }
     }
     THETIS_TRY(check_cuda(lp, "build: keys"));

@@ -312,19 +312,6 @@ struct TileCols {
     int a, ncols;
 };
 
-__device__ __forceinline__ TileCols load_cols(const DevLP& L, int64_t tile, WarpSmem& sm, int lane) {
-    TileCols tc;
-    tc.u0 = tile * 32;
-    int b;
-    scalar_lanes(L, tc.u0, tc.a, b);
-    tc.ncols = b - tc.a;
-    tc.j0 = L.n_blocks * L.k + (tc.u0 + tc.a - L.n_blocks);
-    if (tc.ncols > 0)
-        for (int i = lane; i <= tc.ncols; i += 32) sm.cp[i] = L.colptr[tc.j0 + i];
-    __syncwarp();
-    return tc;
-}
-
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -342,8 +329,9 @@ __device__ __forceinline__ int col_of(const WarpSmem& sm, int ncols, int64_t t) 
 // partial dots of the tile's columns over the nonzero range [c0, c1), added into
 // sm.acc.  Sub-chunks of 32 lying inside one column accumulate in registers;
 // mixed sub-chunks locate each lane's column and add with shared atomics.
+// (rows below m_defer are left out: the row pass accumulated them into lv)
 __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                             int lane) {
+                                             int lane, int64_t m_defer) {
     constexpr int U = 4; // sub-chunks in flight: their loads are issued before any use
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
@@ -360,7 +348,7 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
         for (int q = 0; q < U; q++) {
             const int64_t t = b0 + 32 * q + lane;
             v[q] = 0.0f;
-            if (t < c1) {
+            if (t < c1 && (int64_t)(raw[q] & kRowMask) >= m_defer) {
                 const float rv = ld_cg(L.r + (raw[q] & kRowMask));
                 v[q] = L.val ? L.val[t] * rv : ((raw[q] & kSignBit) ? -rv : rv);
             }
@@ -378,7 +366,7 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
             const int64_t t = base + lane;
             if (base + 32 <= nb || c1 <= nb) {
                 acc += v[q];
-            } else if (t < c1) {
+            } else if (t < c1 && v[q] != 0.0f) {
                 int col = c;
                 while (sm.cp[col + 1] <= t) col++;
                 atomicAdd(&sm.acc[col], v[q]);
@@ -389,9 +377,10 @@ __device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int n
     if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
     __syncwarp();
 }
-// r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]
+// r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]; rows below
+// m_defer are left out (the next row pass applies d_j there)
 __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                              int lane) {
+                                              int lane, int64_t m_defer) {
     constexpr int U = 4;
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
@@ -413,12 +402,13 @@ __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int 
             }
             const int64_t t = base + lane;
             float d = dc;
-            if (!(base + 32 <= nb || c1 <= nb) && t < c1) {
+            const bool live = t < c1 && (int64_t)(raw[q] & kRowMask) >= m_defer;
+            if (!(base + 32 <= nb || c1 <= nb) && live) {
                 int col = c;
                 while (sm.cp[col + 1] <= t) col++;
                 d = sm.d[col];
             }
-            if (t < c1 && d != 0.0f) {
+            if (live && d != 0.0f) {
                 const float a = L.val ? L.val[t] : ((raw[q] & kSignBit) ? -1.0f : 1.0f);
                 red_add(L.r + (raw[q] & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
             }
@@ -427,12 +417,12 @@ __device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int 
 }
 
 // the coordinate step of lane's column from D = sm.acc[lane]; returns the change
+// (z, c: the column's value and cost, loaded ahead by prefetch_tile)
 __device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P, const TileCols& tc, float D,
-                                             int lane) {
+                                             int lane, float z, float c) {
     if (lane >= tc.ncols || (L.unit_fixed && L.unit_fixed[tc.u0 + tc.a + lane])) return 0.0f;
     const int64_t j = tc.j0 + lane;
-    float z = L.z[j];
-    float g = grad_fast(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta, P.inv_beta);
+    float g = grad_fast(c, ua_of(L, j), D, z, zbar_of(L, j), P.beta, P.inv_beta);
     float invL = unit_invL(P, col_norm2(L, j));
     float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
     L.z[j] = zn;
@@ -463,7 +453,16 @@ struct HubCtx {
     int n_items;
     unsigned long long* next;    // work item counter
     const int2* pk;              // per-row keys of the row pass (k_pass_keys)
+    float2* lv;                  // per scalar column {D_j from the row pass, pending light step d_j}:
+                                 // a light (non-hub) column's rows with a hub endpoint
+    int64_t m_defer;             // rows [0, m_defer) have a hub endpoint (R-17)
 };
+// row-pass keys: >= 0 a hub slot (or, for .x in a shared item, the index into the
+// range's shared arrays); <= -2 the light column -(k + 2); -1 nothing
+__device__ __forceinline__ float* key_acc(const HubCtx& H, int k) {
+    return k >= 0 ? (float*)H.hv + 2 * (int64_t)k : (float*)H.lv - 2 * ((int64_t)k + 2);
+}
+__device__ __forceinline__ float key_pend(const HubCtx& H, int k) { return __ldg(key_acc(H, k) + 1); }
 __device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int32_t v) {
     const int32_t h = H.hub_id[v >> 5];
     return h < 0 ? -1 : h * 32 + (v & 31);
@@ -490,19 +489,19 @@ constexpr int kPassThreads = 1024;             // one block per SM, shared d / D
 constexpr int64_t kItemRows = 1 << 19;         // rows per work item
 constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side through global memory
 
-// v-side of a row: rows come in runs of equal max endpoint (equal slot key, -1 =
-// not a hub); add the warp's run segments with one atomic each.  Fast path when
-// the whole warp is one run.
-__device__ __forceinline__ void add_max_side(float* acc, int key, float val, int lane, bool skip = false) {
+// v-side of a row: rows come in runs of equal max endpoint (equal key, -1 = none);
+// add the warp's run segments with one atomic each.  Fast path when the whole warp
+// is one run.
+__device__ __forceinline__ void add_max_side(const HubCtx& H, int key, float val, int lane, bool skip = false) {
     const int k0 = __shfl_sync(0xffffffffu, key, 0);
     if (__all_sync(0xffffffffu, key == k0)) {
-        if (k0 < 0) return;
+        if (k0 == -1) return;
 #pragma unroll
         for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        if (lane == 0 && !skip) atomicAdd(acc + k0, val);
+        if (lane == 0 && !skip) atomicAdd(key_acc(H, k0), val);
         return;
     }
-    float sv = key >= 0 ? val : 0.0f;
+    float sv = key != -1 ? val : 0.0f;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const float x = __shfl_down_sync(0xffffffffu, sv, o);
@@ -510,19 +509,27 @@ __device__ __forceinline__ void add_max_side(float* acc, int key, float val, int
         if (lane + o < 32 && k2 == key) sv += x;
     }
     const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-    if (key >= 0 && (lane == 0 || prev != key) && !skip) atomicAdd(acc + key, sv);
+    if (key != -1 && (lane == 0 || prev != key) && !skip) atomicAdd(key_acc(H, key), sv);
 }
 
 // per-row keys of the row pass, built once per solve: .x = the min endpoint's
-// index in its range's shared arrays (rows of shared items) or its global slot
-// (other rows), .y = the max endpoint's global slot; -1 = not a hub column
+// index in its range's shared arrays (rows of shared items) or its global key (other
+// rows), .y = the max endpoint's global key; rows without a hub endpoint: (-1, -1)
+__device__ __forceinline__ int32_t global_key(const HubCtx& H, int32_t v) {
+    const int32_t h = hub_slot(H, v);
+    return h >= 0 ? h : H.lv ? -(v + 2) : -1;
+}
 __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range_shared, int2* __restrict__ pk) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
+        if (e >= H.m_defer) {
+            pk[e] = make_int2(-1, -1);
+            continue;
+        }
         const int2 uv = L.edges[e];
         const int32_t g = uv.x >> kRowRangeShift;
-        int32_t su = hub_slot(H, uv.x);
-        if (su >= 0 && e < L.m_hub_rows && range_shared[g]) su = uv.x - (g << kRowRangeShift);
-        pk[e] = make_int2(su, hub_slot(H, uv.y));
+        const int32_t gu = global_key(H, uv.x);
+        const int32_t su = gu != -1 && e < L.m_hub_rows && range_shared[g] ? uv.x - (g << kRowRangeShift) : gu;
+        pk[e] = make_int2(su, global_key(H, uv.y));
     }
 }
 
@@ -548,6 +555,12 @@ __device__ __forceinline__ void fix_add(uint32_t* lo, int32_t* hi, int i, float 
 __device__ __forceinline__ float fix_value(uint32_t lo, int32_t hi) {
     return (float)((double)(((long long)hi << 32) | lo) * (1.0 / (double)(1 << kFixShift)));
 }
+#ifndef THETIS_PF_DIST
+#define THETIS_PF_DIST 0
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 template <bool kSlack, bool kAnchor>
 __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepParams P, HubCtx H, int apply, int exp) {
     extern __shared__ float smem[];
@@ -571,19 +584,22 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
         const int it = s_it;
         if (it >= H.n_items) return;
         const int4 w = H.items[it];
+        if (!kSlack && w.y >= H.m_defer) continue;  // no pending step reaches these rows
         const int32_t base = w.x << kRowRangeShift;
         const bool sh = w.w != 0;
         if (sh) {
             for (int t = threadIdx.x; t < kRowRange / 32; t += blockDim.x)
-                s_hub[t] = (int64_t)base + t * 32 < L.n_scalar ? H.hub_id[(base >> 5) + t] : -1;
+                s_hub[t] = (int64_t)base + t * 32 < L.n_scalar ? H.hub_id[(base >> 5) + t] : -2;
             __syncthreads();
             constexpr int kPer = (kRowRange + kPassThreads - 1) / kPassThreads;
             float pv[kPer];
 #pragma unroll
             for (int q = 0; q < kPer; q++) {  // all loads in flight together
                 const int i = threadIdx.x + q * kPassThreads;
-                const int32_t h = i < kRowRange ? s_hub[i >> 5] : -1;
-                pv[q] = apply && h >= 0 ? pend_of(H.hv, h * 32 + (i & 31)) : 0.0f;
+                const int32_t h = i < kRowRange ? s_hub[i >> 5] : -2;  // -2: past the columns
+                pv[q] = !apply || h == -2 || (h < 0 && !H.lv) ? 0.0f
+                        : h >= 0                           ? pend_of(H.hv, h * 32 + (i & 31))
+                                                           : __ldg((const float*)(H.lv + base + i) + 1);
             }
 #pragma unroll
             for (int q = 0; q < kPer; q++) {
@@ -600,6 +616,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
         // the thread first, then across the warp), groups 4-aligned from a0
         const int64_t a0 = w.y & ~(int64_t)3;
         for (int64_t g0 = a0 + 4 * (int64_t)threadIdx.x; g0 - 4 * lane < w.z; g0 += 4 * (int64_t)blockDim.x) {
+#if THETIS_PF_DIST > 0
+            if (lane == 0) {  // L2 bulk prefetch of the warp's rows THETIS_PF_DIST iterations ahead
+                const int64_t pf = g0 + THETIS_PF_DIST * 4 * (int64_t)blockDim.x;
+                if (pf + 128 <= w.z) {
+                    bulk_prefetch_l2(pk + pf, 128 * sizeof(int2));
+                    bulk_prefetch_l2(r + pf, 128 * sizeof(float));
+                    if (kSlack && zvec) bulk_prefetch_l2(zs + pf, 128 * sizeof(float));
+                }
+            }
+#endif
             int2 key[4];
             float r0[4], z[4];
             bool ok[4];
@@ -636,10 +662,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             for (int j = 0; j < 4; j++) {
                 float du = 0.0f, dv = 0.0f;
                 if (apply) {
-                    if (key[j].x >= 0) du = sh ? s_pend[key[j].x] : pend_of(H.hv, key[j].x);
-                    if (key[j].y >= 0 && !(exp & 4)) {
+                    if (key[j].x != -1) du = sh ? s_pend[key[j].x] : key_pend(H, key[j].x);
+                    if (key[j].y != -1 && !(exp & 4)) {
                         // the thread's rows are sorted by max endpoint: reuse the previous load
-                        dv = (j > 0 && key[j].y == key[j - 1].y) ? dvp : pend_of(H.hv, key[j].y);
+                        dv = (j > 0 && key[j].y == key[j - 1].y) ? dvp : key_pend(H, key[j].y);
                         dvp = dv;
                     }
                 }
@@ -677,9 +703,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
             if (kSlack) {
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    if (key[j].x >= 0 && !(exp & 2)) {
+                    if (key[j].x != -1 && !(exp & 2)) {
                         if (sh) fix_add(s_lo, s_hi, key[j].x, rv[j]);
-                        else atomicAdd(acc_of(H.hv, key[j].x), rv[j]);
+                        else atomicAdd(key_acc(H, key[j].x), rv[j]);
                     }
                 }
                 if (!(exp & 1)) {
@@ -697,18 +723,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                     if (!b3 && !b2) tail += rv[1];
                     if (single) tail = head;
                     // complete runs strictly inside the thread: {1}, {1, 2} or {2}
-                    if (b1 && b2 && k1 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k1, rv[1]);
-                    if (b1 && !b2 && b3 && k1 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k1, rv[1] + rv[2]);
-                    if (b2 && b3 && k2 >= 0) atomicAdd((float*)H.hv + 2 * (int64_t)k2, rv[2]);
+                    if (b1 && b2 && k1 != -1) atomicAdd(key_acc(H, k1), rv[1]);
+                    if (b1 && !b2 && b3 && k1 != -1) atomicAdd(key_acc(H, k1), rv[1] + rv[2]);
+                    if (b2 && b3 && k2 != -1) atomicAdd(key_acc(H, k2), rv[2]);
                     // a non-single next lane hands its head to my tail when the run continues
                     const int nk0 = __shfl_down_sync(0xffffffffu, key[0].y, 1);
                     const float nh = __shfl_down_sync(0xffffffffu, head, 1);
                     const bool nsingle = __shfl_down_sync(0xffffffffu, (int)single, 1);
                     if (lane < 31 && !nsingle && nk0 == key[3].y) tail += nh;
                     const int pk3 = __shfl_up_sync(0xffffffffu, key[3].y, 1);
-                    if (!single && !(lane > 0 && key[0].y == pk3) && key[0].y >= 0)
-                        atomicAdd((float*)H.hv + 2 * (int64_t)key[0].y, head);
-                    add_max_side((float*)H.hv, key[3].y >= 0 ? 2 * key[3].y : -1, tail, lane, exp & 8);
+                    if (!single && !(lane > 0 && key[0].y == pk3) && key[0].y != -1) atomicAdd(key_acc(H, key[0].y), head);
+                    add_max_side(H, key[3].y, tail, lane, exp & 8);
                 }
             }
         }
@@ -718,7 +743,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                 const int32_t h = s_hub[i >> 5];
                 const uint32_t lo = s_lo[i];
                 const int32_t hi = s_hi[i];
-                if (h >= 0 && (lo | (uint32_t)hi)) atomicAdd(acc_of(H.hv, h * 32 + (i & 31)), fix_value(lo, hi));
+                if ((lo | (uint32_t)hi) && (h >= 0 || H.lv))
+                    atomicAdd(h >= 0 ? acc_of(H.hv, h * 32 + (i & 31)) : (float*)(H.lv + base + i), fix_value(lo, hi));
             }
         }
     }
@@ -748,29 +774,91 @@ struct AsyncCtx {
     int64_t n_tiles, heavy_limit;  // tiles above heavy_limit were done by the hub step
     unsigned long long* next;      // position counters (one per stream, 256 B apart)
     int streams;
+    const int32_t* hub_id;         // per tile: >= 0 for hub tiles (skipped), or null
+    int exp;                       // experiment switches (THETIS_EXP; 0 in production)
+    float2* lv;                    // with a hub step: per scalar column {D from the row pass, pending step}
+    int64_t m_defer;               // rows [0, m_defer) reach the tiles through lv (R-6), others directly
+    const int64_t* ll_off;         // with lv: per scalar column, its rows >= m_defer are
+    const int32_t* ll_row;         //   ll_row[ll_off[j] .. ll_off[j + 1])
 };
+
+// The loads of a tile that do not depend on r, issued one tile ahead: its column
+// starts (lane i: column i; every lane: the end) and the lane's column z and c.
+// z_j has a single writer per epoch (the tile's own worker), so the early read
+// sees the same value as a late one.
+struct TilePre {
+    TileCols tc;
+    int64_t cp, cp_end;
+    float z, c, acc;  // acc: the row pass's part of D (lv), 0 without a hub step
+};
+__device__ __forceinline__ TilePre prefetch_tile(const DevLP& L, const AsyncCtx& C, int64_t tile, int lane) {
+    TilePre t;
+    t.tc.u0 = tile * 32;
+    int b;
+    scalar_lanes(L, t.tc.u0, t.tc.a, b);
+    t.tc.ncols = b - t.tc.a;
+    t.tc.j0 = L.n_blocks * L.k + (t.tc.u0 + t.tc.a - L.n_blocks);
+    t.cp = t.cp_end = 0;
+    t.z = t.c = t.acc = 0.0f;
+    if (t.tc.ncols > 0) {
+        if (lane < t.tc.ncols) {
+            const int64_t j = t.tc.j0 + lane;
+            t.z = L.z[j];
+            t.c = c_int(L, j);
+            if (C.lv) {  // with lv: the lane's own rows >= m_defer
+                t.acc = C.lv[j].x;
+                t.cp = C.ll_off[j];
+                t.cp_end = C.ll_off[j + 1];
+            } else {
+                t.cp = L.colptr[j];
+            }
+        }
+        if (!C.lv) t.cp_end = L.colptr[t.tc.j0 + t.tc.ncols];
+    }
+    return t;
+}
+
+// a light tile with lv (VC / MIS rows, coefficients +1): D = the row pass's part plus
+// the lane's few rows without a hub endpoint; the step reaches the rows with a hub
+// endpoint through the next row pass (lv.y), the others directly
+__device__ __forceinline__ void process_light_tile(const DevLP& L, const StepParams& P, const AsyncCtx& C,
+                                                   const TilePre& t, int lane) {
+    const TileCols& tc = t.tc;
+    float D = t.acc;
+    for (int64_t q = t.cp; q < t.cp_end; q++) D += ld_cg(L.r + C.ll_row[q]);
+    const float d = scalar_step(L, P, tc, D, lane, t.z, t.c);
+    if (lane < tc.ncols) C.lv[tc.j0 + lane] = make_float2(0.0f, d);
+    __syncwarp();  // tile-synchronous: every gather of the tile before any scatter
+    if (d != 0.0f)
+        for (int64_t q = t.cp; q < t.cp_end; q++) red_add(L.r + C.ll_row[q], d);
+}
 
 // (3) One tile of structural units by one warp, tile-synchronous: all units
 // gather (stale w.r.t. other tiles in flight), then all scatter.  A hub tile's
 // scalar range was stepped by the hub step of this epoch and is skipped.
-__device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx& C, int64_t tile, WarpSmem& sm,
-                             int lane) {
-    const int64_t u0 = tile * 32, u = u0 + lane;
-    const bool is_block = u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
+template <bool kBlocks>
+__device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx& C, const TilePre& t,
+                             WarpSmem& sm, int lane) {
+    const TileCols& tc = t.tc;
+    const int64_t u = tc.u0 + lane;
+    const bool is_block = kBlocks && u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
     float xb[kMaxK];
     if (is_block) block_values(L, P, u, xb);
-    TileCols tc = load_cols(L, tile, sm, lane);
     unsigned moved = 0;
     int64_t beg = 0, end = 0;
     if (tc.ncols > 0) {
-        beg = sm.cp[0];
-        end = sm.cp[tc.ncols];
+        beg = __shfl_sync(0xffffffffu, t.cp, 0);
+        end = t.cp_end;
         if (end - beg <= C.heavy_limit) {
-            sm.acc[lane] = 0.0f;
+            if (lane < tc.ncols) sm.cp[lane] = t.cp;
+            if (lane == 0) sm.cp[tc.ncols] = end;
+            sm.acc[lane] = t.acc;
             __syncwarp();
-            gather_range(L, sm, tc.ncols, beg, end, lane);
-            const float d = scalar_step(L, P, tc, sm.acc[lane], lane);
+            if (!(C.exp & 16)) gather_range(L, sm, tc.ncols, beg, end, lane, C.m_defer);
+            const float d = scalar_step(L, P, tc, sm.acc[lane], lane, t.z, t.c);
             sm.d[lane] = d;
+            // the row pass applies d to the rows below m_defer and accumulates D anew
+            if (C.lv && lane < tc.ncols) C.lv[tc.j0 + lane] = make_float2(0.0f, d);
             moved = __ballot_sync(0xffffffffu, d != 0.0f);
         }
     }
@@ -783,15 +871,23 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
             L.z[j] = xb[l];
         }
     }
-    if (moved) scatter_range(L, sm, tc.ncols, beg, end, lane);
+    if (moved && !(C.exp & 32)) scatter_range(L, sm, tc.ncols, beg, end, lane, C.m_defer);
     __syncwarp();
 }
 
 // Persistent, one warp = one worker: draw the next `batch` positions of the
 // permuted tile sequence (a stream = a contiguous part of the sequence; one
 // stream unless the grid is large) and process them.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async(DevLP L, StepParams P, AsyncCtx C, int batch,
-                                                               int64_t n_workers) {
+// resident blocks per SM: the tile loop is latency-bound, so the VC / MIS variant is
+// held to few registers for high occupancy; the block variant keeps its
+// registers (its simplex arrays would spill); 6 blocks (40 registers) measured best
+#ifndef THETIS_ASYNC_MINB
+#define THETIS_ASYNC_MINB 6
+#endif
+// kBlocks: the LP has simplex blocks (MWC); without them the block path is compiled out
+template <bool kBlocks>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kBlocks ? 1 : THETIS_ASYNC_MINB) k_async(DevLP L, StepParams P, AsyncCtx C,
+                                                                                 int batch, int64_t n_workers) {
     __shared__ WarpSmem wsm[kWarpsPerBlock];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& sm = wsm[w];
@@ -811,10 +907,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_async(DevLP L, StepPara
             continue;
         }
         // the batch's permuted tiles, one Feistel evaluation per lane
-        const int64_t mine = lane < batch && first + lane < hi ? (int64_t)tile_perm((uint64_t)(first + lane), C.K) : 0;
-        for (int i = 0; i < batch && first + i < hi; i++) {
-            const int64_t tile = __shfl_sync(0xffffffffu, mine, i);
-            process_tile(L, P, C, tile, sm, lane);
+        const bool mine_ok = lane < batch && first + lane < hi;
+        const int64_t mine = mine_ok ? (int64_t)tile_perm((uint64_t)(first + lane), C.K) : 0;
+        // hub tiles were stepped by the hub step of this epoch: drop them up front
+        unsigned todo = __ballot_sync(0xffffffffu, mine_ok && !(C.hub_id && C.hub_id[mine] >= 0));
+        if (!todo) continue;
+        TilePre cur = prefetch_tile(L, C, __shfl_sync(0xffffffffu, mine, __ffs(todo) - 1), lane);
+        while (todo) {
+            todo &= todo - 1;
+            TilePre nxt = cur;  // the next tile's loads go out before this tile's work
+            if (todo) nxt = prefetch_tile(L, C, __shfl_sync(0xffffffffu, mine, __ffs(todo) - 1), lane);
+            if (!kBlocks && C.lv) process_light_tile(L, P, C, cur, lane);
+            else process_tile<kBlocks>(L, P, C, cur, sm, lane);
+            cur = nxt;
         }
     }
 }
@@ -832,6 +937,27 @@ __global__ void k_find_heavy(DevLP L, int64_t n_tiles, int64_t limit, int32_t* h
         }
         flags[tile] = hv;
         if (hv) heavy[atomicAdd(count, 1ull)] = (int32_t)tile;
+    }
+}
+
+// the rows >= m_defer of every light scalar column (lv mode): counts, then the list
+__global__ void k_ll_count(DevLP L, const int32_t* __restrict__ hub_id, int64_t m_defer, int64_t* __restrict__ cnt) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < L.n_scalar; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = 0;
+        if (hub_id[j >> 5] < 0)
+            for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) c += (int64_t)(L.rowidx[t] & kRowMask) >= m_defer;
+        cnt[j] = c;
+    }
+}
+__global__ void k_ll_fill(DevLP L, const int32_t* __restrict__ hub_id, int64_t m_defer, const int64_t* __restrict__ off,
+                          int32_t* __restrict__ rows) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < L.n_scalar; j += (int64_t)gridDim.x * blockDim.x) {
+        if (hub_id[j >> 5] >= 0) continue;
+        int64_t o = off[j];
+        for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) {
+            const int32_t row = (int32_t)(L.rowidx[t] & kRowMask);
+            if (row >= m_defer) rows[o++] = row;
+        }
     }
 }
 
@@ -854,17 +980,18 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 // once (< 0.8% of the tiles), and never more than the device holds (persistent
 // grid); large LPs are bounded by the device, not by the depth.
 constexpr int64_t kAsyncDepth = 128;
-static int64_t async_workers(int64_t n_tiles) {
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
+static int64_t async_workers(int64_t n_tiles, bool blocks) {
+    static int per_sm[2] = {0, 0}, sms = 0;
+    if (!per_sm[blocks]) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async, kWarpsPerBlock * 32, 0);
-        if (per_sm < 1) per_sm = 1;
+        if (blocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_async<true>, kWarpsPerBlock * 32, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_async<false>, kWarpsPerBlock * 32, 0);
+        if (per_sm[blocks] < 1) per_sm[blocks] = 1;
     }
     int64_t depth_cap = n_tiles / kAsyncDepth;
-    int64_t dev_cap = (int64_t)per_sm * sms * kWarpsPerBlock;
+    int64_t dev_cap = (int64_t)per_sm[blocks] * sms * kWarpsPerBlock;
     int64_t w = depth_cap < dev_cap ? depth_cap : dev_cap;
     return w < 1 ? 1 : w;
 }
@@ -947,7 +1074,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         THETIS_TRY(ensure_heavy(lp));
         H.n_heavy = lp->n_heavy;
         H.heavy_tiles = hub_list(lp);
-        workers = serial ? 1 : async_workers(n_tiles);
+        workers = serial ? 1 : async_workers(n_tiles, L.n_blocks > 0);
         blocks = (workers + kWarpsPerBlock - 1) / kWarpsPerBlock;
         AC.streams = blocks >= 128 ? (int)(blocks / 64) : 1;
         batch = blocks >= 128 ? kBatch : 1;
@@ -965,10 +1092,24 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         uint8_t* range_shared = C.take<uint8_t>(n_ranges + 1);
         int2* pk = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
         H.pk = pk;
+        // light columns reach their rows with a hub endpoint through the row pass (R-6);
+        // keys -(v + 2) must fit int32
+        const bool defer = H.n_heavy > 0 && L.n_scalar < (int64_t)INT32_MAX - 2 && L.n_blocks == 0;
+        H.lv = defer ? C.take<float2>(L.n_scalar) : nullptr;
+        H.m_defer = defer ? L.m_defer_rows : L.m;  // without lv every row keeps its hub keys
+        int64_t* ll_off = defer ? C.take<int64_t>(L.n_scalar + 1) : nullptr;
+        int32_t* ll_row = nullptr;
+        size_t ll_cub = 0;
+        void* ll_cubp = nullptr;
+        if (defer) {
+            cub::DeviceScan::ExclusiveSum(nullptr, ll_cub, ll_off, ll_off, L.n_scalar + 1);
+            ll_cubp = C.take<char>((int64_t)ll_cub);
+        }
         if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp");
         if (H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(hub_id, 0xFF, (size_t)n_tiles * 4, s));
             CUDA_TRY(lp, cudaMemsetAsync(H.hv, 0, (size_t)H.n_heavy * 32 * 8, s));
+            if (H.lv) CUDA_TRY(lp, cudaMemsetAsync(H.lv, 0, (size_t)L.n_scalar * 8, s));
             k_hub_ids<<<grid_for(H.n_heavy, 256), 256, 0, s>>>(H.n_heavy, H.heavy_tiles, hub_id);
             // work items of the row pass: ranges of min endpoints, split into chunks
             // of kItemRows; consecutive small ranges merge into one global-memory item
@@ -1000,10 +1141,27 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 CUDA_TRY(lp, cudaMemcpyAsync(items, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
             CUDA_TRY(lp, cudaMemcpyAsync(range_shared, rsh.data(), rsh.size(), cudaMemcpyHostToDevice, s));
             k_pass_keys<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, range_shared, pk);
+            if (H.lv) {  // the light columns' rows without a hub endpoint
+                CUDA_TRY(lp, cudaMemsetAsync(ll_off + L.n_scalar, 0, 8, s));
+                k_ll_count<<<grid_for(L.n_scalar, 256), 256, 0, s>>>(L, hub_id, H.m_defer, ll_off);
+                CUDA_TRY(lp, cub::DeviceScan::ExclusiveSum(ll_cubp, ll_cub, ll_off, ll_off, L.n_scalar + 1, s));
+                int64_t n_ll = 0;
+                CUDA_TRY(lp, cudaMemcpyAsync(&n_ll, ll_off + L.n_scalar, 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(lp, cudaStreamSynchronize(s));
+                ll_row = C.take<int32_t>(n_ll > 0 ? n_ll : 1);
+                if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async temp (ll)");
+                k_ll_fill<<<grid_for(L.n_scalar, 256), 256, 0, s>>>(L, hub_id, H.m_defer, ll_off, ll_row);
+            }
             CUDA_TRY(lp, cudaStreamSynchronize(s));  // `it`, `rsh` are pageable host memory
         }
         AC.n_tiles = n_tiles;
         AC.heavy_limit = hub_step_enabled(L) ? kHeavy : INT64_MAX;
+        AC.hub_id = H.n_heavy > 0 ? H.hub_id : nullptr;
+        AC.lv = H.lv;
+        AC.m_defer = H.lv ? H.m_defer : 0;
+        AC.ll_off = ll_off;
+        AC.ll_row = ll_row;
+        AC.exp = g_exp;
         hub_blocks = pass_blocks();
         anchored = L.zbar != nullptr || L.ubar != nullptr;
     }
@@ -1051,7 +1209,8 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (n_tiles > 0) {
                 CUDA_TRY(lp, cudaMemsetAsync(AC.next, 0, (size_t)AC.streams * 32 * 8, s));
                 AC.K = make_perm_keys(n_tiles, seed, e);
-                k_async<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                if (L.n_blocks > 0) k_async<true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                else k_async<false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
         }
         if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) THETIS_TRY(kern_mark(e, 2));

@@ -7,7 +7,7 @@ import sys
 rows = list(csv.reader(open(sys.argv[1])))
 units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0   # e.g. rows / 32 -> per warp-row
 hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r != hdr and r[0] != hdr[0]]
 agg, st = collections.Counter(), collections.Counter()
 for d in data:
     src = re.sub(r"^@!?U?P\w+\s+", "", d["Source"].strip())
