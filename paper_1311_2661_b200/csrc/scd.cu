@@ -453,15 +453,14 @@ struct HubCtx {
     int n_items;
     unsigned long long* next;    // work item counter
     const int2* pk;              // per-row keys of the row pass (k_pass_keys)
-    float2* lv;                  // per scalar column {D_j from the row pass, pending light step d_j}:
-                                 // a light (non-hub) column's rows with a hub endpoint
+    float2* lv;                  // hv + 32 n_heavy: per scalar column {D_j from the row pass, pending
+                                 // light step d_j}: a light column's rows with a hub endpoint
     int64_t m_defer;             // rows [0, m_defer) have a hub endpoint (R-17)
 };
-// row-pass keys: >= 0 a hub slot (or, for .x in a shared item, the index into the
-// range's shared arrays); <= -2 the light column -(k + 2); -1 nothing
-__device__ __forceinline__ float* key_acc(const HubCtx& H, int k) {
-    return k >= 0 ? (float*)H.hv + 2 * (int64_t)k : (float*)H.lv - 2 * ((int64_t)k + 2);
-}
+// row-pass keys: an entry of hv (hub slots, then with lv the light columns: lv = hv +
+// 32 n_heavy) or, for .x in a shared item, the index into the range's shared arrays;
+// -1 nothing
+__device__ __forceinline__ float* key_acc(const HubCtx& H, int k) { return (float*)H.hv + 2 * (int64_t)k; }
 __device__ __forceinline__ float key_pend(const HubCtx& H, int k) { return __ldg(key_acc(H, k) + 1); }
 __device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int32_t v) {
     const int32_t h = H.hub_id[v >> 5];
@@ -517,7 +516,7 @@ __device__ __forceinline__ void add_max_side(const HubCtx& H, int key, float val
 // rows), .y = the max endpoint's global key; rows without a hub endpoint: (-1, -1)
 __device__ __forceinline__ int32_t global_key(const HubCtx& H, int32_t v) {
     const int32_t h = hub_slot(H, v);
-    return h >= 0 ? h : H.lv ? -(v + 2) : -1;
+    return h >= 0 ? h : H.lv ? (int32_t)(H.n_heavy * 32) + v : -1;
 }
 __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range_shared, int2* __restrict__ pk) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
@@ -540,26 +539,37 @@ __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range
 // kAnchor: the LP has anchors (zbar / ubar), else both are zero.  The slack step
 // is slack_new<true> written out for graph rows (sigma = sg for every row).
 constexpr int kPassRows = 4;
-// shared memory: d of the range (float) and the min side of D as 64-bit fixed point
-// (scale 2^kFixShift) split into unsigned low / signed high words, so that the
-// additions are native integer shared atomics (a float add is a CAS loop)
+// shared memory: d of the range (float) and the min side of D in fixed point with
+// resolution 2^-22, kept as two integer sums so that every addition is one native
+// shared atomic without a carry (a float add is a CAS loop): x 2^22 = h 2^12 + l with
+// h = floor(x 2^10) (signed) and l in [0, 2^12].  An item holds <= 2^19 rows, so
+// neither sum can wrap for |x| < 4; larger values go to the global accumulator.
 constexpr size_t kPassSmem = 3 * kRowRange * sizeof(float);
-constexpr int kFixShift = 24;
-__device__ __forceinline__ void fix_add(uint32_t* lo, int32_t* hi, int i, float x) {
-    const long long v = __float2ll_rn(__fmul_rn(x, (float)(1 << kFixShift)));
-    const uint32_t l = (uint32_t)v;
-    const uint32_t old = atomicAdd(lo + i, l);
-    const int32_t h = (int32_t)(v >> 32) + (old + l < old ? 1 : 0);
-    if (h) atomicAdd(hi + i, h);
+constexpr float kFixBound = 4.0f;
+__device__ __forceinline__ bool fix_add(uint32_t* lo, int32_t* hi, int i, float x) {
+    if (!(fabsf(x) < kFixBound)) return false;
+    const float t = x * 1024.0f;                       // exact (power of two)
+    const float f = floorf(t);
+    atomicAdd(hi + i, (int32_t)f);
+    atomicAdd(lo + i, (uint32_t)__float2int_rn((t - f) * 4096.0f));  // t - f exact, in [0, 1)
+    return true;
 }
 __device__ __forceinline__ float fix_value(uint32_t lo, int32_t hi) {
-    return (float)((double)(((long long)hi << 32) | lo) * (1.0 / (double)(1 << kFixShift)));
+    return (float)(((double)hi * 4096.0 + (double)lo) * (1.0 / 4194304.0));
 }
-#ifndef THETIS_PF_DIST
-#define THETIS_PF_DIST 0
-#endif
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// the keys of rows g .. g + 3 of item w ((-1, -1) outside it)
+__device__ __forceinline__ void load_keys4(const int2* __restrict__ pk, int64_t m, const int4& w, int64_t g, int4& k01,
+                                           int4& k23) {
+    if (g + 4 <= m && g >= w.y && g + 4 <= w.z) {
+        k01 = __ldcs((const int4*)(pk + g));
+        k23 = __ldcs((const int4*)(pk + g + 2));
+        return;
+    }
+    int2 k[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) k[j] = g + j >= w.y && g + j < w.z ? __ldcs(pk + g + j) : make_int2(-1, -1);
+    k01 = make_int4(k[0].x, k[0].y, k[1].x, k[1].y);
+    k23 = make_int4(k[2].x, k[2].y, k[3].x, k[3].y);
 }
 template <bool kSlack, bool kAnchor>
 __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepParams P, HubCtx H, int apply, int exp) {
@@ -599,7 +609,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                 const int32_t h = i < kRowRange ? s_hub[i >> 5] : -2;  // -2: past the columns
                 pv[q] = !apply || h == -2 || (h < 0 && !H.lv) ? 0.0f
                         : h >= 0                           ? pend_of(H.hv, h * 32 + (i & 31))
-                                                           : __ldg((const float*)(H.lv + base + i) + 1);
+                                                           : pend_of(H.lv, base + i);
             }
 #pragma unroll
             for (int q = 0; q < kPer; q++) {
@@ -616,23 +626,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
         // the thread first, then across the warp), groups 4-aligned from a0
         const int64_t a0 = w.y & ~(int64_t)3;
         for (int64_t g0 = a0 + 4 * (int64_t)threadIdx.x; g0 - 4 * lane < w.z; g0 += 4 * (int64_t)blockDim.x) {
-#if THETIS_PF_DIST > 0
-            if (lane == 0) {  // L2 bulk prefetch of the warp's rows THETIS_PF_DIST iterations ahead
-                const int64_t pf = g0 + THETIS_PF_DIST * 4 * (int64_t)blockDim.x;
-                if (pf + 128 <= w.z) {
-                    bulk_prefetch_l2(pk + pf, 128 * sizeof(int2));
-                    bulk_prefetch_l2(r + pf, 128 * sizeof(float));
-                    if (kSlack && zvec) bulk_prefetch_l2(zs + pf, 128 * sizeof(float));
-                }
-            }
-#endif
             int2 key[4];
+            {
+                int4 k01, k23;
+                load_keys4(pk, L.m, w, g0, k01, k23);
+                key[0] = make_int2(k01.x, k01.y); key[1] = make_int2(k01.z, k01.w);
+                key[2] = make_int2(k23.x, k23.y); key[3] = make_int2(k23.z, k23.w);
+            }
             float r0[4], z[4];
             bool ok[4];
             if (g0 + 4 <= L.m && g0 >= w.y && g0 + 4 <= w.z) {
-                const int4 k01 = __ldcs((const int4*)(pk + g0)), k23 = __ldcs((const int4*)(pk + g0 + 2));
-                key[0] = make_int2(k01.x, k01.y); key[1] = make_int2(k01.z, k01.w);
-                key[2] = make_int2(k23.x, k23.y); key[3] = make_int2(k23.z, k23.w);
                 const float4 rr = __ldcs((const float4*)(r + g0));
                 r0[0] = rr.x; r0[1] = rr.y; r0[2] = rr.z; r0[3] = rr.w;
                 if (kSlack) {
@@ -651,7 +654,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                 for (int j = 0; j < 4; j++) {
                     const int64_t e = g0 + j;
                     ok[j] = e >= w.y && e < w.z;
-                    key[j] = ok[j] ? __ldcs(pk + e) : make_int2(-1, -1);
                     r0[j] = ok[j] ? __ldcs(r + e) : 0.0f;
                     z[j] = kSlack && ok[j] ? __ldcs(zs + e) : 0.0f;
                 }
@@ -704,8 +706,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     if (key[j].x != -1 && !(exp & 2)) {
-                        if (sh) fix_add(s_lo, s_hi, key[j].x, rv[j]);
-                        else atomicAdd(key_acc(H, key[j].x), rv[j]);
+                        if (!sh) atomicAdd(key_acc(H, key[j].x), rv[j]);
+                        else if (!fix_add(s_lo, s_hi, key[j].x, rv[j])) {
+                            const int i = key[j].x, h = s_hub[i >> 5];
+                            atomicAdd(h >= 0 ? acc_of(H.hv, h * 32 + (i & 31)) : acc_of(H.lv, base + i), rv[j]);
+                        }
                     }
                 }
                 if (!(exp & 1)) {
@@ -744,7 +749,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_rows_pass(DevLP L, StepPara
                 const uint32_t lo = s_lo[i];
                 const int32_t hi = s_hi[i];
                 if ((lo | (uint32_t)hi) && (h >= 0 || H.lv))
-                    atomicAdd(h >= 0 ? acc_of(H.hv, h * 32 + (i & 31)) : (float*)(H.lv + base + i), fix_value(lo, hi));
+                    atomicAdd(h >= 0 ? acc_of(H.hv, h * 32 + (i & 31)) : acc_of(H.lv, base + i), fix_value(lo, hi));
             }
         }
     }
@@ -1082,7 +1087,11 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         AC.next = C.take<unsigned long long>(32 * (int64_t)AC.streams);
         int32_t* hub_id = C.take<int32_t>(n_tiles);
         H.hub_id = hub_id;
-        H.hv = C.take<float2>(H.n_heavy * 32);
+        // light columns reach their rows with a hub endpoint through the row pass (R-6):
+        // their accumulators follow the hub slots in hv (keys must fit int32)
+        const bool defer = H.n_heavy > 0 && H.n_heavy * 32 + L.n_scalar < (int64_t)INT32_MAX && L.n_blocks == 0;
+        H.hv = C.take<float2>(H.n_heavy * 32 + (defer ? L.n_scalar : 0));
+        H.lv = defer ? H.hv + H.n_heavy * 32 : nullptr;
         H.next = C.take<unsigned long long>(32 * 2);
         const int64_t n_ranges = (L.n_scalar + kRowRange - 1) / kRowRange;
         int32_t* rstart = C.take<int32_t>(n_ranges + 1);
@@ -1092,10 +1101,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         uint8_t* range_shared = C.take<uint8_t>(n_ranges + 1);
         int2* pk = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
         H.pk = pk;
-        // light columns reach their rows with a hub endpoint through the row pass (R-6);
-        // keys -(v + 2) must fit int32
-        const bool defer = H.n_heavy > 0 && L.n_scalar < (int64_t)INT32_MAX - 2 && L.n_blocks == 0;
-        H.lv = defer ? C.take<float2>(L.n_scalar) : nullptr;
         H.m_defer = defer ? L.m_defer_rows : L.m;  // without lv every row keeps its hub keys
         int64_t* ll_off = defer ? C.take<int64_t>(L.n_scalar + 1) : nullptr;
         int32_t* ll_row = nullptr;

@@ -41,8 +41,11 @@ def main():
     th._check(th.thetis_build_graph_lp_workspace(th.THETIS_PROB_VC, n, E, 0, ctypes.byref(need)), "ws")
     ws = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
     h = ctypes.c_void_p()
+    tev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    tev[0].record(s)
     th._check(th.thetis_build_graph_lp(ctypes.byref(h), ws.data_ptr(), ws.numel(), sp, th.THETIS_PROB_VC, n, E,
                                        src.data_ptr(), dst.data_ptr(), w.data_ptr(), None, 0, None, 0), "build")
+    tev[1].record(s)
     del src, dst
     d = th.Dims()
     th.thetis_get_dims(h, ctypes.byref(d))
@@ -84,9 +87,20 @@ def main():
     eps = list(st.ms_per_epoch[:a.epochs])
     out.update(epoch_ms=sorted(eps)[len(eps) // 2], row_pass_ms=st.ms_row_pass / st.row_pass_launches,
                hub_update_ms=st.ms_hub_update / a.epochs, tiles_ms=st.ms_tiles / a.epochs)
+    tev[2].record(s)
     ob = th.Objective()
     th._check(th.thetis_objective(h, 10.0, ctypes.byref(ob)), "obj", h)
+    tev[3].record(s)
+    sel = torch.empty(n, dtype=torch.uint8, device=dev)
+    rr = th.RoundResult()
+    th._check(th.thetis_round(h, th.THETIS_ROUND_VC_HALF, cfg.round_seed, 1, sel.data_ptr(), ctypes.byref(rr)), "round", h)
+    tev[4].record(s)
+    s.synchronize()
     out["f_beta"] = ob.f_beta
+    out["ms_build"] = tev[0].elapsed_time(tev[1])
+    out["ms_solve_setup_and_epochs"] = tev[1].elapsed_time(tev[2])
+    out["ms_objective"] = tev[2].elapsed_time(tev[3])
+    out["ms_round"] = tev[3].elapsed_time(tev[4])
     th.thetis_free(h)
     print(json.dumps(out))
 
