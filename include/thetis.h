@@ -130,10 +130,10 @@ THETIS_API int thetis_build_graph_lp_workspace(int problem, int64_t n, int64_t n
  *  src, dst   int32[n_edges] endpoints in [0, n); orientation free; self-loops
  *             dropped; duplicate pairs kept once (the first occurrence's
  *             edge weight is used).  Rows follow the unique canonical pairs
- *             (u < v) (R-17): VC / MIS rows whose larger endpoint v
- *             lies in a hub tile (32 consecutive ids with > 512 incidences)
- *             first, sorted by (u >> 14, v, u); then the other rows (all MWC
- *             rows) sorted by (v, u).  Each CSC column lists the rows where the
+ *             (u < v) (R-17): VC / MIS rows with an endpoint in a
+ *             hub tile (32 consecutive ids with > 512 incidences) first, sorted
+ *             by (u >> 14, v, u); then the other rows (all MWC rows) sorted by
+ *             (v, u).  Each CSC column lists the rows where the
  *             vertex is the larger endpoint, then those where it is the smaller,
  *             each in ascending row order.  n must satisfy
  *             ((n-2) >> 14) * n * 2^14 + ... < 2^64 (n <= 2^32), else

@@ -312,6 +312,15 @@ static int cmp_keyed(const void* a, const void* b) {
     if (x->key != y->key) return x->key < y->key ? -1 : 1;
     return x->idx < y->idx ? -1 : (x->idx > y->idx);
 }
+static int cmp_vranged_key(const void* a, const void* b) { /* (v >> ROW_RANGE_SHIFT, u, v) */
+    const keyed_edge* x = (const keyed_edge*)a;
+    const keyed_edge* y = (const keyed_edge*)b;
+    uint64_t gx = (x->key >> 32) >> ROW_RANGE_SHIFT, gy = (y->key >> 32) >> ROW_RANGE_SHIFT;
+    if (gx != gy) return gx < gy ? -1 : 1;
+    uint64_t ux = x->key & 0xFFFFFFFFu, uy = y->key & 0xFFFFFFFFu;
+    if (ux != uy) return ux < uy ? -1 : 1;
+    return (x->key >> 32) < (y->key >> 32) ? -1 : ((x->key >> 32) > (y->key >> 32));
+}
 static int cmp_plain_key(const void* a, const void* b) { /* (v, u); keys are unique here */
     const keyed_edge* x = (const keyed_edge*)a;
     const keyed_edge* y = (const keyed_edge*)b;
@@ -351,8 +360,8 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
     {
         /* R-17: the rows whose larger endpoint lies in a hub tile (VC / MIS: a tile
          * of 32 vertices with more than HUB_NNZ incidences) keep this order; then the
-         * other rows whose smaller endpoint lies in a hub tile, sorted by (v, u);
-         * then the remaining rows, sorted by (v, u) */
+         * other rows whose smaller endpoint lies in a hub tile, sorted by
+         * (v >> ROW_RANGE_SHIFT, u, v); then the remaining rows, sorted by (v, u) */
         int64_t n_tiles = (n + 31) / 32;
         int64_t* tnz = (int64_t*)xcalloc(n_tiles + 1, sizeof(int64_t));
         for (int64_t e = 0; e < me; e++) {
@@ -372,7 +381,7 @@ int thetis_ref_build_graph_lp(ref_lp** out, int problem, int64_t n, int64_t n_ed
         for (int64_t e = 0; e < me; e++)
             if (!(hubs && tnz[(ke[e].key >> 32) >> 5] > HUB_NNZ) && !(hubs && tnz[(ke[e].key & 0xFFFFFFFFu) >> 5] > HUB_NNZ))
                 ord[q++] = ke[e];
-        qsort(ord + m1, (size_t)(m2 - m1), sizeof(keyed_edge), cmp_plain_key);
+        qsort(ord + m1, (size_t)(m2 - m1), sizeof(keyed_edge), cmp_vranged_key);
         qsort(ord + m2, (size_t)(me - m2), sizeof(keyed_edge), cmp_plain_key);
         memcpy(ke, ord, (size_t)me * sizeof(keyed_edge));
         free(ord);

@@ -6,8 +6,9 @@
 //   the rows with a hub max endpoint, ordered by (u >> kRowRangeShift, v, u) (the
 //   rows whose min endpoint lies in one range of 2^14 ids are contiguous: the row
 //   pass accumulates that side in shared memory; within a range a vertex's edges to
-//   smaller ids are one run); then the other rows with a hub min endpoint, then the
-//   rest, each in (v, u) order.  MWC: all rows in (v, u) order
+//   smaller ids are one run); then the other rows with a hub min endpoint, ordered
+//   by (v >> kRowRangeShift, u, v) (the same, with the roles of the endpoints
+//   swapped); then the rest in (v, u) order.  MWC: all rows in (v, u) order
 //   VC  (Eq. 2):   row e = (u < v): x_u + x_v - s_e = 1
 //   MIS (App. B.2):           row e:           x_u + x_v + s_e = 1, max w^T x
 //   MWC (App. B.3): x_v^l at v*k+l, x_e^l at n*k+e*k+l;
@@ -130,27 +131,38 @@ struct HubMaxRow {  // the row's max endpoint lies in a hub tile; row = (min, ma
     const int32_t* cnt;
     __device__ __forceinline__ bool operator()(uint64_t row) const { return cnt[(int32_t)(row >> 32) >> 5] > kHeavy; }
 };
-// rows with a light max endpoint (R-17): key = (light(u) n + v) n + u, i.e. the rows
-// with a hub min endpoint first, each part in (v, u) order; counts the first part
-__global__ void k_plain_keys(int64_t m, int64_t n, const int2* __restrict__ rows, const int32_t* __restrict__ cnt,
-                             uint64_t* __restrict__ keys, unsigned long long* n_hub_min) {
+// rows with a light max endpoint (R-17): those with a hub min endpoint first, in
+// (v >> kRowRangeShift, u, v) order: key = ((v >> shift) n + u) 2^shift + (v mod 2^shift)
+// < ka; then the others in (v, u) order: key = ka + v n + u.  Counts the first part.
+__global__ void k_light_keys(int64_t m, int64_t n, uint64_t ka, const int2* __restrict__ rows,
+                             const int32_t* __restrict__ cnt, uint64_t* __restrict__ keys, unsigned long long* n_a) {
     unsigned long long c = 0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         const int2 uv = rows[e];
-        const bool hub_u = cnt[uv.x >> 5] > kHeavy;
-        c += hub_u;
-        keys[e] = ((hub_u ? 0ull : (uint64_t)n) + (uint64_t)uv.y) * (uint64_t)n + (uint64_t)uv.x;
+        const uint64_t u = (uint64_t)uv.x, v = (uint64_t)uv.y;
+        if (cnt[uv.x >> 5] > kHeavy) {
+            c++;
+            keys[e] = (((v >> kRowRangeShift) * (uint64_t)n + u) << kRowRangeShift) | (v & (kRowRange - 1));
+        } else {
+            keys[e] = ka + v * (uint64_t)n + u;
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_hub_min, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_a, c);
 }
-// decode (light(u) n + v) n + u
-__global__ void k_decode_plain(int64_t m, int64_t n, const uint64_t* __restrict__ keys, int2* __restrict__ edges) {
+__global__ void k_decode_light(int64_t m, int64_t n, uint64_t ka, const uint64_t* __restrict__ keys,
+                               int2* __restrict__ edges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t k = keys[e];
-        const uint64_t hv = k / (uint64_t)n;
-        edges[e] = make_int2((int32_t)(k - hv * (uint64_t)n), (int32_t)(hv % (uint64_t)n));
+        if (k < ka) {
+            const uint64_t gu = k >> kRowRangeShift;  // (v >> shift) n + u
+            const uint64_t g = gu / (uint64_t)n;
+            edges[e] = make_int2((int32_t)(gu - g * (uint64_t)n), (int32_t)((g << kRowRangeShift) | (k & (kRowRange - 1))));
+        } else {
+            const uint64_t q = k - ka, v = q / (uint64_t)n;
+            edges[e] = make_int2((int32_t)(q - v * (uint64_t)n), (int32_t)v);
+        }
     }
 }
 
@@ -446,7 +458,12 @@ static unsigned __int128 graph_key_end(int64_t n) {
     const unsigned __int128 nn = (unsigned __int128)n, u = nn - 2, v = nn - 1;
     return ((((u >> kRowRangeShift) * nn + v)) << kRowRangeShift) + (u & (kRowRange - 1)) + 1;
 }
-bool graph_keys_fit(int64_t n) { return graph_key_end(n) <= (unsigned __int128)UINT64_MAX; }
+bool graph_keys_fit(int64_t n) {
+    // also the keys of the rows with a light max endpoint (k_light_keys): ka + n^2
+    const unsigned __int128 nn = (unsigned __int128)(n > 0 ? n : 1);
+    const unsigned __int128 ka = (((nn - 1) >> kRowRangeShift) + 1) * nn << kRowRangeShift;
+    return graph_key_end(n) <= (unsigned __int128)UINT64_MAX && ka + nn * nn <= (unsigned __int128)UINT64_MAX;
+}
 uint64_t graph_key_sentinel(int64_t n) { return (uint64_t)graph_key_end(n); }
 
 int bits_for(uint64_t v) {
@@ -773,8 +790,8 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
     d.m_hub_rows = 0;
     d.m_defer_rows = 0;
     if (!mwc && m > 0) {
-        // ---- R-17 hub partition: rows with a hub max endpoint keep the ranged order,
-        // the others follow in (max, min) order
+        // ---- R-17 hub partition: rows with a hub max endpoint keep the ranged order;
+        // then the rows with a hub min endpoint, ranged by the max endpoint; then the rest
         int32_t* tcnt = t.us;  // n_tiles <= n counters, rewritten below
         const int64_t n_tiles = (n + 31) / 32;
         CUDA_TRY(lp, cudaMemsetAsync(tcnt, 0, (size_t)n_tiles * 4, s));
@@ -790,13 +807,14 @@ int build_graph(thetis_lp* lp, int problem, int64_t n, int64_t E, const int32_t*
         const int64_t m2 = m - m1;
         if (m1 > 0) CUDA_TRY(lp, cudaMemcpyAsync((void*)d.edges, part, (size_t)m1 * 8, cudaMemcpyDeviceToDevice, s));
         if (m2 > 0) {
+            const uint64_t ka = ((((uint64_t)n - 1) >> kRowRangeShift) + 1) * (uint64_t)n << kRowRangeShift;
             CUDA_TRY(lp, cudaMemsetAsync(t.nsel, 0, 8, s));
-            k_plain_keys<<<grid_for(m2, T), T, 0, s>>>(m2, n, (const int2*)(part + m1), tcnt, t.keys2,
+            k_light_keys<<<grid_for(m2, T), T, 0, s>>>(m2, n, ka, (const int2*)(part + m1), tcnt, t.keys2,
                                                        (unsigned long long*)t.nsel);
             cub::DoubleBuffer<uint64_t> dk(t.keys2, t.keys);
             cb = t.cub_bytes;
-            CUDA_TRY(lp, sort_keys_u64(t.cub, cb, dk, m2, bits_for(2 * (uint64_t)n * (uint64_t)n), s));
-            k_decode_plain<<<grid_for(m2, T), T, 0, s>>>(m2, n, dk.Current(), (int2*)d.edges + m1);
+            CUDA_TRY(lp, sort_keys_u64(t.cub, cb, dk, m2, bits_for(ka + (uint64_t)n * (uint64_t)n), s));
+            k_decode_light<<<grid_for(m2, T), T, 0, s>>>(m2, n, ka, dk.Current(), (int2*)d.edges + m1);
             int64_t ma = 0;
             CUDA_TRY(lp, cudaMemcpyAsync(&ma, t.nsel, 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));

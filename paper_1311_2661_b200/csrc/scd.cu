@@ -472,12 +472,14 @@ __global__ void k_hub_ids(int64_t n_heavy, const int32_t* heavy_tiles, int32_t* 
         hub_id[heavy_tiles[h]] = (int32_t)h;
 }
 // first row of every range of min endpoints (rows are sorted by range): lower bound
-__global__ void k_range_starts(DevLP L, int64_t n_ranges, int32_t* start) {
+// (rows [r0, r1) ranged by their min (side 0) or max (side 1) endpoint)
+__global__ void k_range_starts(DevLP L, int64_t r0, int64_t r1, int side, int64_t n_ranges, int32_t* start) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= n_ranges; g += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = 0, hi = L.m_hub_rows;
+        int64_t lo = r0, hi = r1;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            if ((int64_t)(L.edges[mid].x >> kRowRangeShift) < g) lo = mid + 1;
+            const int2 uv = L.edges[mid];
+            if ((int64_t)((side ? uv.y : uv.x) >> kRowRangeShift) < g) lo = mid + 1;
             else hi = mid;
         }
         start[g] = (int32_t)lo;
@@ -487,6 +489,7 @@ __global__ void k_range_starts(DevLP L, int64_t n_ranges, int32_t* start) {
 constexpr int kPassThreads = 1024;             // one block per SM, shared d / D of one range
 constexpr int64_t kItemRows = 1 << 19;         // rows per work item
 constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side through global memory
+constexpr int64_t kSharedMinRowsA = 1 << 12;   // the same for the ranges of the rows with a hub min endpoint only
 
 // v-side of a row: rows come in runs of equal max endpoint (equal key, -1 = none);
 // add the warp's run segments with one atomic each.  Fast path when the whole warp
@@ -518,17 +521,22 @@ __device__ __forceinline__ int32_t global_key(const HubCtx& H, int32_t v) {
     const int32_t h = hub_slot(H, v);
     return h >= 0 ? h : H.lv ? (int32_t)(H.n_heavy * 32) + v : -1;
 }
-__global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range_shared, int2* __restrict__ pk) {
+// .x is the ranged endpoint (rows [0, m_hub_rows): the min one; rows [m_hub_rows,
+// m_defer_rows): the max one), .y the other
+__global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range_shared,
+                            const uint8_t* __restrict__ range_shared_a, int2* __restrict__ pk) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < L.m; e += (int64_t)gridDim.x * blockDim.x) {
         if (e >= H.m_defer) {
             pk[e] = make_int2(-1, -1);
             continue;
         }
         const int2 uv = L.edges[e];
-        const int32_t g = uv.x >> kRowRangeShift;
-        const int32_t gu = global_key(H, uv.x);
-        const int32_t su = gu != -1 && e < L.m_hub_rows && range_shared[g] ? uv.x - (g << kRowRangeShift) : gu;
-        pk[e] = make_int2(su, global_key(H, uv.y));
+        const bool a = e >= L.m_hub_rows && e < L.m_defer_rows;
+        const int32_t x = a ? uv.y : uv.x, y = a ? uv.x : uv.y;
+        const int32_t g = x >> kRowRangeShift;
+        const int32_t gx = global_key(H, x);
+        const bool sh = gx != -1 && e < L.m_defer_rows && (a ? range_shared_a[g] : range_shared[g]);
+        pk[e] = make_int2(sh ? x - (g << kRowRangeShift) : gx, global_key(H, y));
     }
 }
 
@@ -1094,11 +1102,11 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         H.lv = defer ? H.hv + H.n_heavy * 32 : nullptr;
         H.next = C.take<unsigned long long>(32 * 2);
         const int64_t n_ranges = (L.n_scalar + kRowRange - 1) / kRowRange;
-        int32_t* rstart = C.take<int32_t>(n_ranges + 1);
-        const int64_t max_items = 2 * (L.m / kItemRows) + 2 * n_ranges + 4;
+        int32_t* rstart = C.take<int32_t>(2 * (n_ranges + 1));
+        const int64_t max_items = 2 * (L.m / kItemRows) + 4 * n_ranges + 8;
         int4* items = C.take<int4>(H.n_heavy > 0 ? max_items : 1);
         H.items = items;
-        uint8_t* range_shared = C.take<uint8_t>(n_ranges + 1);
+        uint8_t* range_shared = C.take<uint8_t>(2 * (n_ranges + 1));
         int2* pk = C.take<int2>(H.n_heavy > 0 ? L.m : 1);
         H.pk = pk;
         H.m_defer = defer ? L.m_defer_rows : L.m;  // without lv every row keeps its hub keys
@@ -1116,36 +1124,44 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             CUDA_TRY(lp, cudaMemsetAsync(H.hv, 0, (size_t)H.n_heavy * 32 * 8, s));
             if (H.lv) CUDA_TRY(lp, cudaMemsetAsync(H.lv, 0, (size_t)L.n_scalar * 8, s));
             k_hub_ids<<<grid_for(H.n_heavy, 256), 256, 0, s>>>(H.n_heavy, H.heavy_tiles, hub_id);
-            // work items of the row pass: ranges of min endpoints, split into chunks
+            // work items of the row pass: ranges of the ranged endpoint, split into chunks
             // of kItemRows; consecutive small ranges merge into one global-memory item
-            k_range_starts<<<grid_for(n_ranges + 1, 256), 256, 0, s>>>(L, n_ranges, rstart);
-            std::vector<int32_t> hs(n_ranges + 1);
-            CUDA_TRY(lp, cudaMemcpyAsync(hs.data(), rstart, (size_t)(n_ranges + 1) * 4, cudaMemcpyDeviceToHost, s));
+            const int64_t ma0 = L.m_hub_rows, ma1 = L.m_defer_rows;
+            k_range_starts<<<grid_for(n_ranges + 1, 256), 256, 0, s>>>(L, 0, ma0, 0, n_ranges, rstart);
+            k_range_starts<<<grid_for(n_ranges + 1, 256), 256, 0, s>>>(L, ma0, ma1, 1, n_ranges, rstart + n_ranges + 1);
+            std::vector<int32_t> hs(2 * (n_ranges + 1));
+            CUDA_TRY(lp, cudaMemcpyAsync(hs.data(), rstart, hs.size() * 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));
             std::vector<int4> it;
-            std::vector<uint8_t> rsh(n_ranges + 1, 0);
-            for (int64_t g = 0; g < n_ranges; g++) {
-                const int32_t b0 = hs[g], b1 = hs[g + 1];
-                if (b1 <= b0) continue;
-                if (b1 - b0 >= kSharedMinRows) {
-                    rsh[g] = 1;
-                    for (int64_t p = b0; p < b1; p += kItemRows)
-                        it.push_back(make_int4((int)g, (int)p, (int)(p + kItemRows < b1 ? p + kItemRows : b1), 1));
-                } else if (!it.empty() && it.back().w == 0 && it.back().z == b0 && b1 - it.back().y <= kItemRows) {
-                    it.back().z = b1;
-                } else {
-                    it.push_back(make_int4((int)g, b0, b1, 0));
+            std::vector<uint8_t> rsh(2 * (n_ranges + 1), 0);
+            for (int part = 0; part < 2; part++) {
+                const int32_t* st = hs.data() + part * (n_ranges + 1);
+                uint8_t* sh = rsh.data() + part * (n_ranges + 1);
+                // ranged by the max endpoint: only light columns gain from the shared side
+                const int64_t min_rows = part == 0 ? kSharedMinRows : (H.lv ? kSharedMinRowsA : INT64_MAX);
+                for (int64_t g = 0; g < n_ranges; g++) {
+                    const int32_t b0 = st[g], b1 = st[g + 1];
+                    if (b1 <= b0) continue;
+                    if (b1 - b0 >= min_rows) {
+                        sh[g] = 1;
+                        for (int64_t p = b0; p < b1; p += kItemRows)
+                            it.push_back(make_int4((int)g, (int)p, (int)(p + kItemRows < b1 ? p + kItemRows : b1), 1));
+                    } else if (!it.empty() && it.back().w == 0 && it.back().z == b0 && b1 - it.back().y <= kItemRows) {
+                        it.back().z = b1;
+                    } else {
+                        it.push_back(make_int4((int)g, b0, b1, 0));
+                    }
                 }
             }
-            // rows with a light max endpoint (R-17: after the ranged part): global items
-            for (int64_t p = L.m_hub_rows; p < L.m; p += kItemRows)
+            // rows without a hub endpoint (R-17: the last part): global items
+            for (int64_t p = ma1; p < L.m; p += kItemRows)
                 it.push_back(make_int4(0, (int)p, (int)(p + kItemRows < L.m ? p + kItemRows : L.m), 0));
             if ((int64_t)it.size() > max_items) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "row pass items");
             H.n_items = (int)it.size();
             if (!it.empty())
                 CUDA_TRY(lp, cudaMemcpyAsync(items, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
             CUDA_TRY(lp, cudaMemcpyAsync(range_shared, rsh.data(), rsh.size(), cudaMemcpyHostToDevice, s));
-            k_pass_keys<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, range_shared, pk);
+            k_pass_keys<<<grid_for(L.m, 256), 256, 0, s>>>(L, H, range_shared, range_shared + n_ranges + 1, pk);
             if (H.lv) {  // the light columns' rows without a hub endpoint
                 CUDA_TRY(lp, cudaMemsetAsync(ll_off + L.n_scalar, 0, 8, s));
                 k_ll_count<<<grid_for(L.n_scalar, 256), 256, 0, s>>>(L, hub_id, H.m_defer, ll_off);

@@ -28,9 +28,10 @@ constexpr int kRedThreads = 256;
 struct DevLP {
     int problem, obj_sense, k;
     int64_t m, n_s, n_ineq, N, nnz_s, U, n_blocks, n_scalar, n_vert, m_edges;
-    int64_t m_hub_rows;        // VC / MIS: rows [0, m_hub_rows) have a hub max endpoint (R-17)
-    int64_t m_defer_rows;      // VC / MIS: rows [0, m_defer_rows) have a hub endpoint (R-17): the
-                               // row pass owns them, light steps reach them through it (R-6)
+    int64_t m_hub_rows;        // VC / MIS: rows [0, m_hub_rows) have a hub max endpoint (R-17), ranged by u
+    int64_t m_defer_rows;      // rows [m_hub_rows, m_defer_rows) have a hub min endpoint only, ranged
+                               // by v; rows [0, m_defer_rows) belong to the row pass, light steps reach
+                               // them through it (R-6)
     // A, structural part: CSC, rows ascending.  val == nullptr: coefficient
     // +1, or -1 when bit 31 of rowidx is set.
     const int64_t* colptr;

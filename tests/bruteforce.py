@@ -20,8 +20,8 @@ def unique_edges(n, src, dst):
 def row_order(n, edges, hubs=True, hub_nnz=512):
     """R-17 written out: rows whose larger endpoint lies in a hub tile (32 consecutive
     vertex ids with more than hub_nnz incidences; VC / MIS only) in (u >> 14, v, u)
-    order; then the other rows whose smaller endpoint lies in a hub tile, in (v, u)
-    order; then the remaining rows, in (v, u) order."""
+    order; then the other rows whose smaller endpoint lies in a hub tile, in
+    (v >> 14, u, v) order; then the remaining rows, in (v, u) order."""
     tnz = {}
     for u, v in edges:
         tnz[u >> 5] = tnz.get(u >> 5, 0) + 1
@@ -33,7 +33,7 @@ def row_order(n, edges, hubs=True, hub_nnz=512):
     first = [e for e in edges if hub(e[1])]
     mixed = [e for e in edges if not hub(e[1]) and hub(e[0])]
     rest = [e for e in edges if not hub(e[1]) and not hub(e[0])]
-    return (sorted(first, key=lambda e: (e[0] >> 14, e[1], e[0])) + sorted(mixed, key=lambda e: (e[1], e[0]))
+    return (sorted(first, key=lambda e: (e[0] >> 14, e[1], e[0])) + sorted(mixed, key=lambda e: (e[1] >> 14, e[0], e[1]))
             + sorted(rest, key=lambda e: (e[1], e[0])))
 
 

@@ -286,13 +286,13 @@ def test_graph_row_order_and_incidence(problem):
     if problem != MWC:
         assert want != sorted(edges, key=lambda e: (e[1], e[0]))  # the hub part is non-empty
         assert want != sorted(edges, key=lambda e: (e[0] >> 14, e[1], e[0]))
-        # the rows with a hub min endpoint and a light max endpoint come before the rest
-        mixed = [e for e in want[:-1] if e[0] < 32 or 20000 <= e[0] < 20032]
-        assert mixed and want.index(mixed[-1]) < len(want) - 1
-        first_light = next(i for i, e in enumerate(want) if not (e[1] < 32 or 20000 <= e[1] < 20032))
-        tail = want[first_light:]
-        k = sum(1 for e in tail if e[0] < 32 or 20000 <= e[0] < 20032)
-        assert 0 < k < len(tail) and all(e[0] < 32 or 20000 <= e[0] < 20032 for e in tail[:k])
+        # three parts: hub max endpoint; hub min endpoint only (ranged by the max endpoint);
+        # the rest
+        hub = lambda x: x < 32 or 20000 <= x < 20032  # noqa: E731
+        part = [0 if hub(e[1]) else 1 if hub(e[0]) else 2 for e in want]
+        assert part == sorted(part) and set(part) == {0, 1, 2}
+        mixed = [e for e, p in zip(want, part) if p == 1]
+        assert mixed == sorted(mixed, key=lambda e: (e[1] >> 14, e[0], e[1])) != sorted(mixed, key=lambda e: (e[1], e[0]))
     assert list(zip(eu.tolist(), ev.tolist())) == want
     if problem != MWC:
         colptr, rowidx, _ = lp.csc()

@@ -1,0 +1,87 @@
+"""Per-config epoch throughput on one B200 (GPU box only; writes one JSON line per run).
+
+For each BASELINE.json config: build the LP through the C ABI from the seeded recipe
+(configs 1-4 generated on the host, config 5 on the device), solve with the config's
+beta and epochs, and report the median epoch time (CUDA events on the solve stream),
+coordinate updates/s, nonzeros/s and the algorithmic bytes per epoch of SURVEY 8(d)
+(20 n_s + 12 nnz_s + 16 m) over the measured HBM peak.  Deterministic mode runs a
+bounded number of epochs where its per-class launches are slow (power-law colourings).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+RUNS = [  # (config, mode, epochs cap)
+    ("vc_er_1k", 0, None), ("vc_er_1k", 1, None),
+    ("mis_er_1m", 0, None), ("mis_er_1m", 1, None),
+    ("vc_chunglu_10m", 0, 3), ("vc_chunglu_10m", 1, None),
+    ("mwc_grid_2048", 0, None), ("mwc_grid_2048", 1, None),
+    ("vc_rmat_26", 1, None),
+]
+PROBLEM = {"vc_er_1k": 1, "mis_er_1m": 2, "vc_chunglu_10m": 1, "mwc_grid_2048": 3, "vc_rmat_26": 1}
+
+
+def main():
+    import torch
+
+    import inputs
+    import paper_1311_2661_b200 as th
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default=None)
+    a = ap.parse_args()
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+    peak = float(peaks["hbm_gbs"])
+    dev = torch.device("cuda", 0)
+    cache = {}
+    for name, mode, cap in RUNS:
+        if a.only and a.only not in name:
+            continue
+        cfg = inputs.CONFIGS[name]
+        prob = PROBLEM[name]
+        if name == "vc_rmat_26":
+            p = cfg.params
+            n, E = 1 << p["scale"], p["samples"]
+            src = torch.empty(E, dtype=torch.int32, device=dev)
+            dst = torch.empty(E, dtype=torch.int32, device=dev)
+            w = torch.empty(n, dtype=torch.float32, device=dev)
+            sp = torch.cuda.current_stream(dev).cuda_stream
+            inputs.rmat_device(p["scale"], E, p["a"], p["b"], p["c"], cfg.graph_seed, src.data_ptr(), dst.data_ptr(), sp)
+            inputs.uniform_weights_device(n, cfg.weight_seed, w.data_ptr(), sp)
+            lp = th.LP.from_graph(prob, n, src, dst, vertex_w=w, device=dev)
+            del src, dst
+        else:
+            g = cache.get(name) or inputs.make_graph(cfg)
+            cache = {name: g}
+            if prob == 3:
+                lp = th.LP.from_graph(prob, g.n, g.src, g.dst, edge_w=g.edge_w, k=g.k, terminals=g.terminals,
+                                      t_per_label=g.t_per_label, device=dev)
+            else:
+                lp = th.LP.from_graph(prob, g.n, g.src, g.dst, vertex_w=g.vertex_w, device=dev)
+        epochs = cfg.epochs if cap is None else min(cap, cfg.epochs)
+        st = lp.solve(cfg.beta, epochs, mode=mode, seed=cfg.solve_seed)
+        ms = st["ms_per_epoch"]
+        med = statistics.median(ms[1:] if len(ms) > 2 else ms)
+        upd = st["coordinate_updates"] / max(st["epochs"], 1)
+        nnz = st["nnz_processed"] / max(st["epochs"], 1)
+        alg = 20 * lp.n_struct + 12 * lp.nnz_struct + 16 * lp.n_ineq
+        ob = lp.objective(cfg.beta)
+        out = dict(config=name, mode="det" if mode == 0 else "async", epochs=epochs, ms_epoch_median=med,
+                   ms_epoch_first=ms[0], updates_per_s=upd / med * 1e3, nnz_per_s=nnz / med * 1e3,
+                   alg_bytes_per_epoch=alg, alg_GBps=alg / med / 1e6, frac_of_measured_hbm=alg / med / 1e6 / peak,
+                   colours=st["n_colours"], n_struct=lp.n_struct, m=lp.m, nnz_struct=lp.nnz_struct,
+                   f_beta=ob["f_beta"], drift_inf=ob["drift_inf"],
+                   ms_row_pass=st["ms_row_pass"] / max(st["row_pass_launches"], 1),
+                   ms_hub_update=st["ms_hub_update"] / epochs, ms_tiles=st["ms_tiles"] / epochs)
+        print(json.dumps(out), flush=True)
+        del lp
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
