@@ -846,6 +846,43 @@ __device__ __forceinline__ void process_light_tile(const DevLP& L, const StepPar
         for (int64_t q = t.cp; q < t.cp_end; q++) red_add(L.r + C.ll_row[q], d);
 }
 
+// A tile of short scalar columns without lv: one lane per column walks its own CSC
+// range (kLaneCol entries at most; the loads of eight entries go out together)
+constexpr int kLaneCol = 48;
+__device__ __forceinline__ bool lane_tile(const TilePre& t, int lane, int64_t& cb, int64_t& ce) {
+    const int64_t nx = __shfl_down_sync(0xffffffffu, t.cp, 1);
+    cb = t.cp;
+    ce = lane + 1 < t.tc.ncols ? nx : (lane + 1 == t.tc.ncols ? t.cp_end : t.cp);
+    if (lane >= t.tc.ncols) ce = cb;
+    return __reduce_max_sync(0xffffffffu, (unsigned)(ce - cb)) <= (unsigned)kLaneCol;
+}
+__device__ __forceinline__ float entry_val(const DevLP& L, int64_t t, uint32_t raw) {
+    return L.val ? L.val[t] : ((raw & kSignBit) ? -1.0f : 1.0f);
+}
+__device__ __forceinline__ void process_lane_tile(const DevLP& L, const StepParams& P, const TilePre& t, int lane,
+                                                  int64_t cb, int64_t ce) {
+    float D = 0.0f;
+    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+        uint32_t raw[8];
+        float rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) raw[u] = q0 + u < ce ? (uint32_t)L.rowidx[q0 + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; u++) rv[u] = q0 + u < ce ? ld_cg(L.r + (raw[u] & kRowMask)) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (q0 + u < ce) D += L.val ? L.val[q0 + u] * rv[u] : ((raw[u] & kSignBit) ? -rv[u] : rv[u]);
+    }
+    const float d = scalar_step(L, P, t.tc, D, lane, t.z, t.c);
+    __syncwarp();  // tile-synchronous: every gather of the tile before any scatter
+    if (d != 0.0f)
+        for (int64_t q = cb; q < ce; q++) {
+            const uint32_t raw = (uint32_t)L.rowidx[q];
+            const float a = entry_val(L, q, raw);
+            red_add(L.r + (raw & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
+        }
+}
+
 // (3) One tile of structural units by one warp, tile-synchronous: all units
 // gather (stale w.r.t. other tiles in flight), then all scatter.  A hub tile's
 // scalar range was stepped by the hub step of this epoch and is skipped.
@@ -897,10 +934,13 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
 #ifndef THETIS_ASYNC_MINB
 #define THETIS_ASYNC_MINB 6
 #endif
-// kBlocks: the LP has simplex blocks (MWC); without them the block path is compiled out
-template <bool kBlocks>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, kBlocks ? 1 : THETIS_ASYNC_MINB) k_async(DevLP L, StepParams P, AsyncCtx C,
-                                                                                 int batch, int64_t n_workers) {
+// kPath: kPathBlocks (the LP has simplex blocks: MWC), kPathScalar (scalar columns,
+// no lv: lane-per-column or warp-cooperative tiles), kPathLight (light tiles with lv)
+enum { kPathBlocks = 0, kPathScalar = 1, kPathLight = 2 };
+template <int kPath>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? 1 : THETIS_ASYNC_MINB)
+    k_async(DevLP L, StepParams P, AsyncCtx C, int batch, int64_t n_workers) {
+    constexpr bool kBlocks = kPath == kPathBlocks;
     __shared__ WarpSmem wsm[kWarpsPerBlock];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& sm = wsm[w];
@@ -930,7 +970,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kBlocks ? 1 : THETIS_ASYN
             todo &= todo - 1;
             TilePre nxt = cur;  // the next tile's loads go out before this tile's work
             if (todo) nxt = prefetch_tile(L, C, __shfl_sync(0xffffffffu, mine, __ffs(todo) - 1), lane);
-            if (!kBlocks && C.lv) process_light_tile(L, P, C, cur, lane);
+            int64_t cb, ce;
+            if (kPath == kPathLight) process_light_tile(L, P, C, cur, lane);
+            else if (kPath == kPathScalar && lane_tile(cur, lane, cb, ce)) process_lane_tile(L, P, cur, lane, cb, ce);
             else process_tile<kBlocks>(L, P, C, cur, sm, lane);
             cur = nxt;
         }
@@ -993,18 +1035,19 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 // once (< 0.8% of the tiles), and never more than the device holds (persistent
 // grid); large LPs are bounded by the device, not by the depth.
 constexpr int64_t kAsyncDepth = 128;
-static int64_t async_workers(int64_t n_tiles, bool blocks) {
-    static int per_sm[2] = {0, 0}, sms = 0;
-    if (!per_sm[blocks]) {
+static int64_t async_workers(int64_t n_tiles, int path) {
+    static int per_sm[3] = {0, 0, 0}, sms = 0;
+    if (!per_sm[path]) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (blocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_async<true>, kWarpsPerBlock * 32, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_async<false>, kWarpsPerBlock * 32, 0);
-        if (per_sm[blocks] < 1) per_sm[blocks] = 1;
+        if (path == kPathBlocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks>, kWarpsPerBlock * 32, 0);
+        else if (path == kPathScalar) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathScalar>, kWarpsPerBlock * 32, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathLight>, kWarpsPerBlock * 32, 0);
+        if (per_sm[path] < 1) per_sm[path] = 1;
     }
     int64_t depth_cap = n_tiles / kAsyncDepth;
-    int64_t dev_cap = (int64_t)per_sm[blocks] * sms * kWarpsPerBlock;
+    int64_t dev_cap = (int64_t)per_sm[path] * sms * kWarpsPerBlock;
     int64_t w = depth_cap < dev_cap ? depth_cap : dev_cap;
     return w < 1 ? 1 : w;
 }
@@ -1081,13 +1124,18 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     AsyncCtx AC{};
     HubCtx H{};
     int64_t blocks = 1, hub_blocks = 1, workers = 1;
+    int path = kPathScalar;
     bool anchored = false;
     int batch = 1;
     if (mode != THETIS_MODE_DETERMINISTIC) {
         THETIS_TRY(ensure_heavy(lp));
         H.n_heavy = lp->n_heavy;
         H.heavy_tiles = hub_list(lp);
-        workers = serial ? 1 : async_workers(n_tiles, L.n_blocks > 0);
+        // light columns reach their rows with a hub endpoint through the row pass (R-6):
+        // their accumulators follow the hub slots in hv (keys must fit int32)
+        const bool defer = H.n_heavy > 0 && H.n_heavy * 32 + L.n_scalar < (int64_t)INT32_MAX && L.n_blocks == 0;
+        path = L.n_blocks > 0 ? kPathBlocks : defer ? kPathLight : kPathScalar;
+        workers = serial ? 1 : async_workers(n_tiles, path);
         blocks = (workers + kWarpsPerBlock - 1) / kWarpsPerBlock;
         AC.streams = blocks >= 128 ? (int)(blocks / 64) : 1;
         batch = blocks >= 128 ? kBatch : 1;
@@ -1095,9 +1143,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         AC.next = C.take<unsigned long long>(32 * (int64_t)AC.streams);
         int32_t* hub_id = C.take<int32_t>(n_tiles);
         H.hub_id = hub_id;
-        // light columns reach their rows with a hub endpoint through the row pass (R-6):
-        // their accumulators follow the hub slots in hv (keys must fit int32)
-        const bool defer = H.n_heavy > 0 && H.n_heavy * 32 + L.n_scalar < (int64_t)INT32_MAX && L.n_blocks == 0;
         H.hv = C.take<float2>(H.n_heavy * 32 + (defer ? L.n_scalar : 0));
         H.lv = defer ? H.hv + H.n_heavy * 32 : nullptr;
         H.next = C.take<unsigned long long>(32 * 2);
@@ -1230,8 +1275,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (n_tiles > 0) {
                 CUDA_TRY(lp, cudaMemsetAsync(AC.next, 0, (size_t)AC.streams * 32 * 8, s));
                 AC.K = make_perm_keys(n_tiles, seed, e);
-                if (L.n_blocks > 0) k_async<true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
-                else k_async<false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                if (path == kPathBlocks) k_async<kPathBlocks><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                else if (path == kPathScalar) k_async<kPathScalar><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                else k_async<kPathLight><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
         }
         if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) THETIS_TRY(kern_mark(e, 2));
