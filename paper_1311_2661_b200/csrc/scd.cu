@@ -279,6 +279,39 @@ __device__ __forceinline__ void scalar_lanes(const DevLP& L, int64_t u0, int& a,
     b = (int)(hi - u0);
 }
 
+// async column dot / scatter with the loads of eight entries in flight together
+__device__ __forceinline__ float col_dot_async(const DevLP& L, int64_t j) {
+    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
+    float D = 0.0f;
+    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+        uint32_t raw[8];
+        float rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) raw[u] = q0 + u < ce ? (uint32_t)L.rowidx[q0 + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; u++) rv[u] = q0 + u < ce ? ld_cg(L.r + (raw[u] & kRowMask)) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (q0 + u < ce) D += L.val ? L.val[q0 + u] * rv[u] : ((raw[u] & kSignBit) ? -rv[u] : rv[u]);
+    }
+    return D;
+}
+__device__ __forceinline__ void col_scatter_async(const DevLP& L, int64_t j, float d) {
+    if (d == 0.0f) return;
+    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
+    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+        uint32_t raw[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) raw[u] = q0 + u < ce ? (uint32_t)L.rowidx[q0 + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (q0 + u < ce) {
+                const float ad = L.val ? __fmul_rn(L.val[q0 + u], d) : ((raw[u] & kSignBit) ? -d : d);
+                red_add(L.r + (raw[u] & kRowMask), ad);
+            }
+    }
+}
+
 // new values of a k-block from the current (possibly stale) residual
 __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P, int64_t u, float* x) {
     const int k = L.k;
@@ -293,7 +326,7 @@ __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P
     const float invL = unit_invL(P, mx);
     for (int l = 0; l < k; l++) {
         int64_t j = f + l;
-        float D = col_dot_seq<true>(L, j);
+        float D = col_dot_async(L, j);
         float g = grad_fast(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta, P.inv_beta);
         y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
     }
@@ -917,7 +950,7 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
         for (int l = 0; l < L.k; l++) {
             const int64_t j = u * L.k + l;
             float d = __fsub_rn(xb[l], L.z[j]);
-            col_scatter<true>(L, j, d);
+            col_scatter_async(L, j, d);
             L.z[j] = xb[l];
         }
     }
@@ -972,7 +1005,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? 1 
             if (todo) nxt = prefetch_tile(L, C, __shfl_sync(0xffffffffu, mine, __ffs(todo) - 1), lane);
             int64_t cb, ce;
             if (kPath == kPathLight) process_light_tile(L, P, C, cur, lane);
-            else if (kPath == kPathScalar && lane_tile(cur, lane, cb, ce)) process_lane_tile(L, P, cur, lane, cb, ce);
+            else if ((kPath == kPathScalar || cur.tc.u0 >= L.n_blocks) && lane_tile(cur, lane, cb, ce))
+                process_lane_tile(L, P, cur, lane, cb, ce);  // (tiles past the blocks are scalar)
             else process_tile<kBlocks>(L, P, C, cur, sm, lane);
             cur = nxt;
         }
