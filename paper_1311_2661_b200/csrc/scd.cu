@@ -125,35 +125,50 @@ __device__ __forceinline__ void update_scalar_seq(const DevLP& L, const StepPara
     L.z[j] = zn;
 }
 
-// Euclidean projection onto the simplex (sort descending, ties: smaller index first)
+// Euclidean projection onto the simplex (sort descending, ties: smaller index first).
+// KC >= k is the compile-time capacity: every loop runs to KC with a guard, so for
+// small blocks the arrays stay in registers; the sorted order comes from ranks
+// (rank_l = #{m : y_m > y_l, or y_m = y_l and m < l}), and the prefix sums add the
+// sorted values one at a time in that order (the same operation sequence as a sort).
+template <int KC>
 __device__ __forceinline__ void project_simplex(const float* y, int k, float* x) {
-    int idx[kMaxK];
-    for (int l = 0; l < k; l++) idx[l] = l;
-    for (int a = 1; a < k; a++) {
-        int cur = idx[a], b = a - 1;
-        while (b >= 0 && y[idx[b]] < y[cur]) { idx[b + 1] = idx[b]; b--; }
-        idx[b + 1] = cur;
+    int rk[KC];
+#pragma unroll
+    for (int l = 0; l < KC; l++) {
+        int c = 0;
+#pragma unroll
+        for (int m = 0; m < KC; m++)
+            if (l < k && m < k && (y[m] > y[l] || (y[m] == y[l] && m < l))) c++;
+        rk[l] = c;
     }
-    float s = 0.0f, s_rho = y[idx[0]];
+    float s = 0.0f, s_rho = 0.0f;
     int rho = 1;
-    for (int i = 1; i <= k; i++) {
-        float u = y[idx[i - 1]];
+#pragma unroll
+    for (int i = 1; i <= KC; i++) {
+        if (i > k) break;
+        float u = 0.0f;
+#pragma unroll
+        for (int l = 0; l < KC; l++)
+            if (l < k && rk[l] == i - 1) u = y[l];
         s = __fadd_rn(s, u);
+        if (i == 1) s_rho = s;
         if (__fsub_rn(u, __fdiv_rn(__fsub_rn(s, 1.0f), (float)i)) > 0.0f) { rho = i; s_rho = s; }
     }
     float tau = __fdiv_rn(__fsub_rn(s_rho, 1.0f), (float)rho);
-    for (int l = 0; l < k; l++) {
-        float v = __fsub_rn(y[l], tau);
-        x[l] = v > 0.0f ? v : 0.0f;
-    }
+#pragma unroll
+    for (int l = 0; l < KC; l++)
+        if (l < k) {
+            float v = __fsub_rn(y[l], tau);
+            x[l] = v > 0.0f ? v : 0.0f;
+        }
 }
 
 // k-block (App. E): gradient step on the k columns, then projection on the simplex
-template <bool kAsync>
+template <bool kAsync, int KC>
 __device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParams& P, int64_t u) {
     const int k = L.k;
     const int64_t f = u * k;
-    float y[kMaxK], x[kMaxK];
+    float y[KC], x[KC];
     double mx = 0.0;
     if (P.rule == THETIS_STEP_LJ)
         for (int l = 0; l < k; l++) {
@@ -161,19 +176,23 @@ __device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParam
             mx = q > mx ? q : mx;
         }
     const float invL = unit_invL(P, mx);
-    for (int l = 0; l < k; l++) {
-        int64_t j = f + l;
-        float D = col_dot_seq<kAsync>(L, j);
-        float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
-        y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
-    }
-    project_simplex(y, k, x);
-    for (int l = 0; l < k; l++) {
-        int64_t j = f + l;
-        float d = __fsub_rn(x[l], L.z[j]);
-        col_scatter<kAsync>(L, j, d);
-        L.z[j] = x[l];
-    }
+#pragma unroll
+    for (int l = 0; l < KC; l++)
+        if (l < k) {
+            int64_t j = f + l;
+            float D = col_dot_seq<kAsync>(L, j);
+            float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
+            y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
+        }
+    project_simplex<KC>(y, k, x);
+#pragma unroll
+    for (int l = 0; l < KC; l++)
+        if (l < k) {
+            int64_t j = f + l;
+            float d = __fsub_rn(x[l], L.z[j]);
+            col_scatter<kAsync>(L, j, d);
+            L.z[j] = x[l];
+        }
 }
 
 // slack of row i (column j): a = sigma_i e_i, cost 0, bounds [0, inf); the new
@@ -206,6 +225,7 @@ __device__ __forceinline__ void update_slack(const DevLP& L, const StepParams& P
 // ------------------------------------------------------------ deterministic
 // one colour class: members are structural units; long scalar columns are
 // finished by their warp cooperatively with the same sequential summation order
+template <int KC>
 __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const int32_t* __restrict__ members,
                                                    int64_t count) {
     const int lane = threadIdx.x & 31;
@@ -216,7 +236,7 @@ __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const 
     bool deferred = false;
     if (u >= 0) {
         if (u < L.n_blocks) {
-            update_block_seq<false>(L, P, u);
+            update_block_seq<false, KC>(L, P, u);
         } else {
             int64_t j = L.n_blocks * L.k + (u - L.n_blocks);
             if (L.colptr[j + 1] - L.colptr[j] > kDetWarpCol) deferred = true;
@@ -313,10 +333,11 @@ __device__ __forceinline__ void col_scatter_async(const DevLP& L, int64_t j, flo
 }
 
 // new values of a k-block from the current (possibly stale) residual
+template <int KC>
 __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P, int64_t u, float* x) {
     const int k = L.k;
     const int64_t f = u * k;
-    float y[kMaxK];
+    float y[KC];
     double mx = 0.0;
     if (P.rule == THETIS_STEP_LJ)
         for (int l = 0; l < k; l++) {
@@ -324,13 +345,15 @@ __device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P
             mx = q > mx ? q : mx;
         }
     const float invL = unit_invL(P, mx);
-    for (int l = 0; l < k; l++) {
-        int64_t j = f + l;
-        float D = col_dot_async(L, j);
-        float g = grad_fast(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta, P.inv_beta);
-        y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
-    }
-    project_simplex(y, k, x);
+#pragma unroll
+    for (int l = 0; l < KC; l++)
+        if (l < k) {
+            int64_t j = f + l;
+            float D = col_dot_async(L, j);
+            float g = grad_fast(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta, P.inv_beta);
+            y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
+        }
+    project_simplex<KC>(y, k, x);
 }
 
 // per-warp shared state
@@ -919,14 +942,14 @@ __device__ __forceinline__ void process_lane_tile(const DevLP& L, const StepPara
 // (3) One tile of structural units by one warp, tile-synchronous: all units
 // gather (stale w.r.t. other tiles in flight), then all scatter.  A hub tile's
 // scalar range was stepped by the hub step of this epoch and is skipped.
-template <bool kBlocks>
+template <bool kBlocks, int KC>
 __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx& C, const TilePre& t,
                              WarpSmem& sm, int lane) {
     const TileCols& tc = t.tc;
     const int64_t u = tc.u0 + lane;
     const bool is_block = kBlocks && u < L.n_blocks && !(L.unit_fixed && L.unit_fixed[u]);
-    float xb[kMaxK];
-    if (is_block) block_values(L, P, u, xb);
+    float xb[KC];
+    if (is_block) block_values<KC>(L, P, u, xb);
     unsigned moved = 0;
     int64_t beg = 0, end = 0;
     if (tc.ncols > 0) {
@@ -947,12 +970,14 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
     }
     __syncwarp();
     if (is_block) {
-        for (int l = 0; l < L.k; l++) {
-            const int64_t j = u * L.k + l;
-            float d = __fsub_rn(xb[l], L.z[j]);
-            col_scatter_async(L, j, d);
-            L.z[j] = xb[l];
-        }
+#pragma unroll
+        for (int l = 0; l < KC; l++)
+            if (l < L.k) {
+                const int64_t j = u * L.k + l;
+                float d = __fsub_rn(xb[l], L.z[j]);
+                col_scatter_async(L, j, d);
+                L.z[j] = xb[l];
+            }
     }
     if (moved && !(C.exp & 32)) scatter_range(L, sm, tc.ncols, beg, end, lane, C.m_defer);
     __syncwarp();
@@ -969,9 +994,10 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
 #endif
 // kPath: kPathBlocks (the LP has simplex blocks: MWC), kPathScalar (scalar columns,
 // no lv: lane-per-column or warp-cooperative tiles), kPathLight (light tiles with lv)
-enum { kPathBlocks = 0, kPathScalar = 1, kPathLight = 2 };
-template <int kPath>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? 1 : THETIS_ASYNC_MINB)
+enum { kPathBlocks = 0, kPathScalar = 1, kPathLight = 2, kPathBlocks8 = 3 /* host side: blocks, k <= 8 */ };
+// KC: block capacity (kPathBlocks: 8 for k <= 8, registers; kMaxK otherwise)
+template <int kPath, int KC = 1>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? (KC <= 8 ? 3 : 1) : THETIS_ASYNC_MINB)
     k_async(DevLP L, StepParams P, AsyncCtx C, int batch, int64_t n_workers) {
     constexpr bool kBlocks = kPath == kPathBlocks;
     __shared__ WarpSmem wsm[kWarpsPerBlock];
@@ -1007,7 +1033,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? 1 
             if (kPath == kPathLight) process_light_tile(L, P, C, cur, lane);
             else if ((kPath == kPathScalar || cur.tc.u0 >= L.n_blocks) && lane_tile(cur, lane, cb, ce))
                 process_lane_tile(L, P, cur, lane, cb, ce);  // (tiles past the blocks are scalar)
-            else process_tile<kBlocks>(L, P, C, cur, sm, lane);
+            else process_tile<kBlocks, KC>(L, P, C, cur, sm, lane);
             cur = nxt;
         }
     }
@@ -1070,12 +1096,15 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 // grid); large LPs are bounded by the device, not by the depth.
 constexpr int64_t kAsyncDepth = 128;
 static int64_t async_workers(int64_t n_tiles, int path) {
-    static int per_sm[3] = {0, 0, 0}, sms = 0;
+    static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
     if (!per_sm[path]) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (path == kPathBlocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks>, kWarpsPerBlock * 32, 0);
+        if (path == kPathBlocks)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks, kMaxK>, kWarpsPerBlock * 32, 0);
+        else if (path == kPathBlocks8)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks, 8>, kWarpsPerBlock * 32, 0);
         else if (path == kPathScalar) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathScalar>, kWarpsPerBlock * 32, 0);
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathLight>, kWarpsPerBlock * 32, 0);
         if (per_sm[path] < 1) per_sm[path] = 1;
@@ -1168,7 +1197,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         // light columns reach their rows with a hub endpoint through the row pass (R-6):
         // their accumulators follow the hub slots in hv (keys must fit int32)
         const bool defer = H.n_heavy > 0 && H.n_heavy * 32 + L.n_scalar < (int64_t)INT32_MAX && L.n_blocks == 0;
-        path = L.n_blocks > 0 ? kPathBlocks : defer ? kPathLight : kPathScalar;
+        path = L.n_blocks > 0 ? (L.k <= 8 ? kPathBlocks8 : kPathBlocks) : defer ? kPathLight : kPathScalar;
         workers = serial ? 1 : async_workers(n_tiles, path);
         blocks = (workers + kWarpsPerBlock - 1) / kWarpsPerBlock;
         AC.streams = blocks >= 128 ? (int)(blocks / 64) : 1;
@@ -1289,7 +1318,8 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         if (mode == THETIS_MODE_DETERMINISTIC) {
             for (int64_t c = 0; c < lp->K; c++) {
                 int64_t beg = lp->class_ptr[c], cnt = lp->class_ptr[c + 1] - beg;
-                if (cnt > 0) k_det_class<<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
+                if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
+                else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
             }
             if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, s>>>(L, P);
         } else {
@@ -1309,7 +1339,8 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (n_tiles > 0) {
                 CUDA_TRY(lp, cudaMemsetAsync(AC.next, 0, (size_t)AC.streams * 32 * 8, s));
                 AC.K = make_perm_keys(n_tiles, seed, e);
-                if (path == kPathBlocks) k_async<kPathBlocks><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                if (path == kPathBlocks8) k_async<kPathBlocks, 8><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
+                else if (path == kPathBlocks) k_async<kPathBlocks, kMaxK><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
                 else if (path == kPathScalar) k_async<kPathScalar><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
                 else k_async<kPathLight><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
