@@ -517,7 +517,23 @@ struct HubCtx {
 // 32 n_heavy) or, for .x in a shared item, the index into the range's shared arrays;
 // -1 nothing
 __device__ __forceinline__ float* key_acc(const HubCtx& H, int k) { return (float*)H.hv + 2 * (int64_t)k; }
-__device__ __forceinline__ float key_pend(const HubCtx& H, int k) { return __ldg(key_acc(H, k) + 1); }
+#ifndef THETIS_PEND_LD
+#define THETIS_PEND_LD 1  // L2-only loads (ld.global.cg): 8.28 vs 8.36 ms with __ldg, 9.36 with L1::no_allocate
+#endif
+__device__ __forceinline__ float key_pend(const HubCtx& H, int k) {
+    const float* p = key_acc(H, k) + 1;
+#if THETIS_PEND_LD == 1
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#elif THETIS_PEND_LD == 2
+    float v;
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 __device__ __forceinline__ int32_t hub_slot(const HubCtx& H, int32_t v) {
     const int32_t h = H.hub_id[v >> 5];
     return h < 0 ? -1 : h * 32 + (v & 31);
@@ -543,7 +559,10 @@ __global__ void k_range_starts(DevLP L, int64_t r0, int64_t r1, int side, int64_
 }
 
 constexpr int kPassThreads = 1024;             // one block per SM, shared d / D of one range
-constexpr int64_t kItemRows = 1 << 19;         // rows per work item
+#ifndef THETIS_ITEM_SHIFT
+#define THETIS_ITEM_SHIFT 19
+#endif
+constexpr int64_t kItemRows = 1 << THETIS_ITEM_SHIFT;  // rows per work item
 constexpr int64_t kSharedMinRows = 1 << 14;    // smaller ranges: min side through global memory
 constexpr int64_t kSharedMinRowsA = 1 << 12;   // the same for the ranges of the rows with a hub min endpoint only
 

@@ -3,17 +3,17 @@
 #include <cstdio>
 #include <cstdint>
 
-template <int THREADS, int ITEMS, typename K, typename V, typename Off>
+template <int THREADS, int ITEMS, typename K, typename V, typename Off, int RB = 8>
 struct Hub {
     using Base = cub::detail::radix::policy_hub<K, V, Off>;
     using P9 = typename Base::Policy900;
     struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, P9> {
         static constexpr bool ONESWEEP = true;
-        static constexpr int ONESWEEP_RADIX_BITS = 8;
-        using HistogramPolicy = cub::AgentRadixSortHistogramPolicy<128, 16, 1, K, 8>;
-        using ExclusiveSumPolicy = cub::AgentRadixSortExclusiveSumPolicy<256, 8>;
+        static constexpr int ONESWEEP_RADIX_BITS = RB;
+        using HistogramPolicy = cub::AgentRadixSortHistogramPolicy<128, 16, 1, K, RB>;
+        using ExclusiveSumPolicy = cub::AgentRadixSortExclusiveSumPolicy<256, RB>;
         using OnesweepPolicy = cub::AgentRadixSortOnesweepPolicy<THREADS, ITEMS, K, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
-                                                                 cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+                                                                 cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, RB>;
         using ScanPolicy = typename P9::ScanPolicy;
         using DownsweepPolicy = typename P9::DownsweepPolicy;
         using AltDownsweepPolicy = typename P9::AltDownsweepPolicy;
@@ -73,12 +73,12 @@ __global__ void fill64(uint64_t* k, int64_t n, int bits) {
         k[i] = h & ((1ull << bits) - 1);
     }
 }
-template <int TH, int IT, typename Off>
+template <int TH, int IT, typename Off, int RB = 8>
 void run_keys(const char* name, uint64_t* k0, uint64_t* k1, int64_t n, int bits, void* tmp, size_t tmpb) {
     cub::DoubleBuffer<uint64_t> dk(k0, k1);
     cub::DoubleBuffer<cub::NullType> none;
     size_t b = 0;
-    using D = cub::DispatchRadixSort<false, uint64_t, cub::NullType, Off, Hub<TH, IT, uint64_t, cub::NullType, Off>>;
+    using D = cub::DispatchRadixSort<false, uint64_t, cub::NullType, Off, Hub<TH, IT, uint64_t, cub::NullType, Off, RB>>;
     D::Dispatch(nullptr, b, dk, none, (Off)n, 0, bits, true, 0);
     if (b > tmpb) { printf("%s: temp %zu too big\n", name, b); return; }
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -101,25 +101,13 @@ int main() {
     cudaMalloc(&k0, n * 4); cudaMalloc(&k1, n * 4); cudaMalloc(&v0, n * 4); cudaMalloc(&v1, n * 4);
     size_t tmpb = (size_t)2 << 30; void* tmp; cudaMalloc(&tmp, tmpb);
     run_stock(k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<384, 17, unsigned long long>("384x17 off64", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<384, 23, uint32_t>("384x23 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<256, 32, uint32_t>("256x32 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<512, 20, uint32_t>("512x20 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<256, 24, uint32_t>("256x24 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<384, 30, uint32_t>("384x30 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<256, 40, uint32_t>("256x40 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<512, 16, uint32_t>("512x16 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<384, 20, uint32_t>("384x20 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
-    run_pairs<448, 20, uint32_t>("448x20 off32", k0, k1, v0, v1, n, bits, tmp, tmpb);
     cudaFree(v0); cudaFree(v1); cudaFree(k0); cudaFree(k1);
     const int64_t E = 1073741824;
     uint64_t *q0, *q1;
     cudaMalloc(&q0, E * 8); cudaMalloc(&q1, E * 8);
     run_keys<256, 32, unsigned long long>("256x32 off64 (current)", q0, q1, E, 52, tmp, tmpb);
     run_keys<256, 32, uint32_t>("256x32 off32", q0, q1, E, 52, tmp, tmpb);
-    run_keys<384, 20, uint32_t>("384x20 off32", q0, q1, E, 52, tmp, tmpb);
-    run_keys<384, 24, uint32_t>("384x24 off32", q0, q1, E, 52, tmp, tmpb);
-    run_keys<256, 40, uint32_t>("256x40 off32", q0, q1, E, 52, tmp, tmpb);
-    run_keys<512, 16, uint32_t>("512x16 off32", q0, q1, E, 52, tmp, tmpb);
+    run_keys<256, 32, unsigned long long, 9>("256x32 rb9", q0, q1, E, 52, tmp, tmpb);
+    run_keys<256, 32, unsigned long long, 10>("256x32 rb10", q0, q1, E, 52, tmp, tmpb);
     return 0;
 }
