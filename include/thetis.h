@@ -119,6 +119,18 @@ typedef struct {
     int32_t problem, obj_sense;
 } thetis_dims;
 
+#define THETIS_MAX_ALM_ROUNDS 64
+
+typedef struct {
+    int64_t rounds;                  /* outer rounds run (inner solves)                         */
+    int64_t epochs_total;            /* inner epochs over all rounds                            */
+    double ms_total;                 /* device time of the inner solves (CUDA events)           */
+    float beta[THETIS_MAX_ALM_ROUNDS];        /* beta_t of round t                               */
+    double eps[THETIS_MAX_ALM_ROUNDS];        /* max structural violation after round t (R-8)   */
+    double resid_inf[THETIS_MAX_ALM_ROUNDS];  /* ||A z - b||_inf after round t                   */
+    double lp_obj[THETIS_MAX_ALM_ROUNDS];     /* c^T x after round t (original sense)            */
+} thetis_alm_stats;
+
 /* ---- build ------------------------------------------------------------ */
 
 /* Workspace bytes for thetis_build_graph_lp on n vertices and n_edges input
@@ -198,6 +210,26 @@ THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uin
 
 /* Fused reductions at the current z (Def. 2, Eq. 5); fp64 results. */
 THETIS_API int thetis_objective(thetis_lp* lp, float beta, thetis_objective_t* out /* host */);
+
+/* The augmented-Lagrangian outer loop ("proximal method of multipliers", §3.4
+ * "Augmented Lagrangian Framework"; R-19): round t solves
+ * f_beta (Eq. 5) with (beta_t, ubar_t, zbar_t) for `inner_epochs` epochs of
+ * thetis_solve (mode, seed + t, step_rule), then measures eps_t (max structural
+ * violation, R-8) and ||A z - b||_inf; it stops when eps_t <= target_eps or after
+ * max_outer rounds, else updates
+ *     ubar_{t+1} = ubar_t - beta_t (A z_t - b)   (the maintained r; fp32, two roundings)
+ *     zbar_{t+1} = z_t                            (structural and slack coordinates)
+ *     beta_{t+1} = beta_t * beta_growth if ||A z_t - b||_inf > ||A z_{t-1} - b||_inf / 2,
+ *                  else beta_t                    (rounded to float)
+ *  ubar  float[m] device, in/out: the multiplier estimate (caller-initialised, e.g. 0)
+ *  zbar  float[N] device, in/out: the proximal anchor (caller-initialised, e.g. 0)
+ *  Both stay registered as the LP's anchors (thetis_set_anchors) on return.
+ *  Errors: INVALID_ARG (null anchors, beta0 <= 0, beta_growth < 1, max_outer < 1 or
+ *  > THETIS_MAX_ALM_ROUNDS, inner_epochs < 0, unknown mode / rule); DIVERGED (a
+ *  non-finite objective); CUDA.  stats (host) may be NULL. */
+THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float beta0, float beta_growth,
+                                int max_outer, int inner_epochs, int mode, uint64_t seed, int step_rule,
+                                double target_eps, thetis_alm_stats* stats);
 
 /* ---- round ------------------------------------------------------------ */
 

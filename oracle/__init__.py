@@ -35,6 +35,11 @@ class RefObjective(ctypes.Structure):
                 ("nonfinite", ctypes.c_int64)]
 
 
+class RefAlm(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("beta", ctypes.c_float * 64), ("eps", ctypes.c_double * 64),
+                ("resid_inf", ctypes.c_double * 64), ("lp_obj", ctypes.c_double * 64)]
+
+
 class RefRound(ctypes.Structure):
     _fields_ = [("cost", ctypes.c_double), ("feasible", ctypes.c_int64),
                 ("n_selected", ctypes.c_int64), ("eps_or_alpha", ctypes.c_double),
@@ -82,6 +87,11 @@ def _load(bits: int):
     L.thetis_ref_solve.argtypes = [vp, f32, i32, i32, ctypes.c_uint64, i32, ctypes.POINTER(RefStats)]
     L.thetis_ref_objective.restype = i32
     L.thetis_ref_objective.argtypes = [vp, f32, ctypes.POINTER(RefObjective)]
+    L.thetis_ref_solve_alm.restype = i32
+    L.thetis_ref_solve_alm.argtypes = [vp, vp, vp, f32, f32, i32, i32, i32, ctypes.c_uint64, i32, ctypes.c_double,
+                                       ctypes.POINTER(RefAlm)]
+    L.thetis_ref_get_anchors.restype = None
+    L.thetis_ref_get_anchors.argtypes = [vp, vp, vp]
     L.thetis_ref_colouring.restype = i64
     L.thetis_ref_colouring.argtypes = [vp, ctypes.c_uint64, vp]
     L.thetis_ref_tile_perm.restype = None
@@ -222,6 +232,25 @@ class RefLP:
         if rc != 0:
             raise OracleError(rc, "thetis_ref_solve")
         return {f: getattr(st, f) for f, _ in RefStats._fields_}
+
+    def solve_alm(self, beta0, beta_growth=2.0, max_outer=10, inner_epochs=50, mode=MODE_DET, seed=0,
+                  step_rule=STEP_LMAX, target_eps=0.0, ubar=None, zbar=None):
+        """the augmented-Lagrangian outer loop (thetis_ref_solve_alm); returns per-round stats"""
+        ub, zb = _arr(ubar, np.float64), _arr(zbar, np.float64)
+        st = RefAlm()
+        rc = self._L.thetis_ref_solve_alm(self._h, _p(ub), _p(zb), beta0, beta_growth, max_outer, inner_epochs,
+                                          mode, seed, step_rule, target_eps, ctypes.byref(st))
+        if rc != 0:
+            raise OracleError(rc, "thetis_ref_solve_alm")
+        n = int(st.rounds)
+        return dict(rounds=n, beta=list(st.beta)[:n], eps=list(st.eps)[:n], resid_inf=list(st.resid_inf)[:n],
+                    lp_obj=list(st.lp_obj)[:n])
+
+    def anchors(self):
+        ub = np.zeros(max(self.m, 1))
+        zb = np.zeros(max(self.N, 1))
+        self._L.thetis_ref_get_anchors(self._h, ub.ctypes.data, zb.ctypes.data)
+        return ub[: self.m], zb[: self.N]
 
     def objective(self, beta):
         o = RefObjective()

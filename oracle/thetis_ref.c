@@ -1132,3 +1132,55 @@ int thetis_ref_round(const ref_lp* lp, int rule, uint64_t seed, int reps, uint8_
     free(x);
     return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* augmented-Lagrangian outer loop (§3.4; R-19)   */
+/* ------------------------------------------------------------------ */
+/* The method of multipliers for Eq. 3 with the proximal term of Eq. 5: the
+ * multiplier estimate moves against the residual, ubar <- ubar - beta (A z - b)
+ * (the step consistent with the -ubar^T (A x - b) term of Eq. 5), the proximal
+ * anchor moves to the last iterate, zbar <- z; beta grows by beta_growth while
+ * the residual does not halve between rounds. */
+void thetis_ref_get_anchors(const ref_lp* lp, double* ubar, double* zbar) {
+    for (int64_t i = 0; i < lp->m; i++) ubar[i] = lp->ubar ? (double)lp->ubar[i] : 0.0;
+    for (int64_t j = 0; j < lp->N; j++) zbar[j] = lp->zbar ? (double)lp->zbar[j] : 0.0;
+}
+int thetis_ref_solve_alm(ref_lp* lp, const double* ubar0, const double* zbar0, float beta0, float beta_growth,
+                         int max_outer, int inner_epochs, int mode, uint64_t seed, int step_rule,
+                         double target_eps, ref_alm_stats* st) {
+    if (!(beta0 > 0) || !(beta_growth >= 1) || max_outer < 1 || max_outer > 64 || inner_epochs < 0)
+        return REF_INVALID_ARG;
+    free(lp->ubar); free(lp->zbar);
+    lp->ubar = (REAL*)xcalloc(lp->m + 1, sizeof(REAL));
+    lp->zbar = (REAL*)xcalloc(lp->N + 1, sizeof(REAL));
+    for (int64_t i = 0; i < lp->m; i++) lp->ubar[i] = ubar0 ? (REAL)ubar0[i] : (REAL)0;
+    for (int64_t j = 0; j < lp->N; j++) lp->zbar[j] = zbar0 ? (REAL)zbar0[j] : (REAL)0;
+    recompute_ua(lp);
+    if (st) memset(st, 0, sizeof(*st));
+    float beta = beta0;
+    double prev_res = INFINITY;
+    for (int t = 0; t < max_outer; t++) {
+        int rc = thetis_ref_solve(lp, beta, inner_epochs, mode, seed + (uint64_t)t, step_rule, NULL);
+        if (rc != REF_OK) return rc;
+        ref_objective ob;
+        rc = thetis_ref_objective(lp, beta, &ob);
+        if (st) {
+            st->rounds = t + 1;
+            st->beta[t] = beta;
+            st->eps[t] = ob.max_violation_eps;
+            st->resid_inf[t] = ob.resid_inf;
+            st->lp_obj[t] = ob.lp_obj;
+        }
+        if (rc != REF_OK) return rc;
+        if (ob.max_violation_eps <= target_eps || t + 1 == max_outer) break;
+        for (int64_t i = 0; i < lp->m; i++) {
+            REAL step = (REAL)beta * lp->r[i]; /* rounded on its own (-ffp-contract=off) */
+            lp->ubar[i] = lp->ubar[i] - step;
+        }
+        for (int64_t j = 0; j < lp->N; j++) lp->zbar[j] = lp->z[j];
+        recompute_ua(lp);
+        if (ob.resid_inf > 0.5 * prev_res) beta = (float)((double)beta * (double)beta_growth);
+        prev_res = ob.resid_inf;
+    }
+    return REF_OK;
+}

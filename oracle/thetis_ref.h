@@ -110,6 +110,23 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                      int step_rule, ref_stats* st);
 int thetis_ref_objective(const ref_lp* lp, float beta, ref_objective* out);
 
+/* augmented-Lagrangian outer loop (§3.4 "Augmented Lagrangian Framework",
+ * P:480-496; R-19), the same rounds as thetis_solve_alm: solve with
+ * (beta_t, ubar_t, zbar_t) for inner_epochs (mode, seed + t); measure; stop when
+ * eps <= target_eps or after max_outer rounds; else ubar -= beta_t r, zbar = z,
+ * beta grows by beta_growth when ||A z - b||_inf did not halve.  ubar0 / zbar0
+ * may be NULL (zero).  Per round: beta, eps, ||r||_inf, c^T x (up to 64 rounds). */
+typedef struct {
+    int64_t rounds;
+    float beta[64];
+    double eps[64], resid_inf[64], lp_obj[64];
+} ref_alm_stats;
+int thetis_ref_solve_alm(ref_lp* lp, const double* ubar0, const double* zbar0, float beta0, float beta_growth,
+                         int max_outer, int inner_epochs, int mode, uint64_t seed, int step_rule,
+                         double target_eps, ref_alm_stats* st);
+/* the current anchors (zero if unset): ubar (m), zbar (N) */
+void thetis_ref_get_anchors(const ref_lp* lp, double* ubar, double* zbar);
+
 /* colouring used by mode 0 for `seed`: colour per unit (slack units = K,
  * fixed units = -1); returns K (the slack class index) */
 int64_t thetis_ref_colouring(ref_lp* lp, uint64_t seed, int32_t* colour_out);

@@ -64,6 +64,16 @@ class RoundResult(ctypes.Structure):
                 ("rounds", ctypes.c_int64)]
 
 
+THETIS_MAX_ALM_ROUNDS = 64
+
+
+class AlmStats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("epochs_total", ctypes.c_int64), ("ms_total", ctypes.c_double),
+                ("beta", ctypes.c_float * THETIS_MAX_ALM_ROUNDS), ("eps", ctypes.c_double * THETIS_MAX_ALM_ROUNDS),
+                ("resid_inf", ctypes.c_double * THETIS_MAX_ALM_ROUNDS),
+                ("lp_obj", ctypes.c_double * THETIS_MAX_ALM_ROUNDS)]
+
+
 class Dims(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in ("m", "n_struct", "N", "U", "nnz_struct", "n_blocks", "block_k",
                                               "m_edges", "n_vertices", "n_ineq")] + \
@@ -86,6 +96,8 @@ _PROTOS = {
     "thetis_get_r": (_i32, [_vp, _vp, _i64]),
     "thetis_solve": (_i32, [_vp, _f32, _i32, _i32, _u64, _i32, ctypes.POINTER(SolveStats)]),
     "thetis_objective": (_i32, [_vp, _f32, ctypes.POINTER(Objective)]),
+    "thetis_solve_alm": (_i32, [_vp, _vp, _vp, _f32, _f32, _i32, _i32, _i32, _u64, _i32, ctypes.c_double,
+                                ctypes.POINTER(AlmStats)]),
     "thetis_round": (_i32, [_vp, _i32, _u64, _i32, _vp, ctypes.POINTER(RoundResult)]),
     "thetis_round_x": (_i32, [_vp, _vp, _i32, _u64, _i32, _vp, ctypes.POINTER(RoundResult)]),
     "thetis_get_csc": (_i32, [_vp, _vp, _vp, _vp]),
@@ -258,6 +270,28 @@ class LP:
         out = {f: getattr(st, f) for f, _ in SolveStats._fields_ if f != "ms_per_epoch"}
         out["ms_per_epoch"] = list(st.ms_per_epoch)[: min(epochs, THETIS_MAX_EPOCH_TIMES)]
         return out
+
+    def solve_alm(self, beta0, beta_growth=2.0, max_outer=10, inner_epochs=50, mode=THETIS_MODE_DETERMINISTIC,
+                  seed=0, step_rule=THETIS_STEP_LMAX, target_eps=0.0, ubar=None, zbar=None):
+        """thetis_solve_alm: the augmented-Lagrangian outer loop; returns (stats, ubar, zbar)
+        with the final anchors (device tensors, also left registered on the LP)."""
+        torch = _torch()
+        ub = torch.zeros(max(self.m, 1), dtype=torch.float32, device=self.device)
+        zb = torch.zeros(max(self.N, 1), dtype=torch.float32, device=self.device)
+        if ubar is not None:
+            ub[: self.m] = _dev_array(ubar, torch.float32, self.device)
+        if zbar is not None:
+            zb[: self.N] = _dev_array(zbar, torch.float32, self.device)
+        self._anchors = (zb, ub)
+        st = AlmStats()
+        rc = thetis_solve_alm(self._h, ub.data_ptr(), zb.data_ptr(), beta0, beta_growth, max_outer, inner_epochs,
+                              mode, seed, step_rule, target_eps, ctypes.byref(st))
+        _check(rc, "thetis_solve_alm", self._h)
+        n = int(st.rounds)
+        out = dict(rounds=n, epochs_total=int(st.epochs_total), ms_total=float(st.ms_total),
+                   beta=list(st.beta)[:n], eps=list(st.eps)[:n], resid_inf=list(st.resid_inf)[:n],
+                   lp_obj=list(st.lp_obj)[:n])
+        return out, ub[: self.m], zb[: self.N]
 
     def objective(self, beta):
         o = Objective()

@@ -233,6 +233,43 @@ THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uin
     return THETIS_OK;
 }
 
+THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float beta0, float beta_growth,
+                                int max_outer, int inner_epochs, int mode, uint64_t seed, int step_rule,
+                                double target_eps, thetis_alm_stats* stats) {
+    if (!lp) return THETIS_ERR_INVALID_ARG;
+    if (!ubar || !zbar || !is_device_ptr(ubar) || !is_device_ptr(zbar) || !(beta0 > 0.0f) || !isfinite(beta0) ||
+        !(beta_growth >= 1.0f) || !isfinite(beta_growth) || max_outer < 1 || max_outer > THETIS_MAX_ALM_ROUNDS ||
+        inner_epochs < 0 ||
+        (mode != THETIS_MODE_DETERMINISTIC && mode != THETIS_MODE_ASYNC && mode != THETIS_MODE_ASYNC_SERIAL) ||
+        (step_rule != THETIS_STEP_LMAX && step_rule != THETIS_STEP_LJ))
+        return set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments to thetis_solve_alm");
+    THETIS_TRY(thetis_set_anchors(lp, zbar, ubar));
+    if (stats) memset(stats, 0, sizeof(*stats));
+    float beta = beta0;
+    double prev_res = INFINITY;
+    for (int t = 0; t < max_outer; t++) {
+        thetis_solve_stats st;
+        THETIS_TRY(solve_epochs(lp, beta, inner_epochs, mode, seed + (uint64_t)t, step_rule, stats ? &st : nullptr));
+        thetis_objective_t ob;
+        const int rc = objective(lp, beta, &ob);
+        if (stats) {
+            stats->rounds = t + 1;
+            stats->epochs_total += inner_epochs;
+            stats->ms_total += st.ms_total;
+            stats->beta[t] = beta;
+            stats->eps[t] = ob.max_violation_eps;
+            stats->resid_inf[t] = ob.resid_inf;
+            stats->lp_obj[t] = ob.lp_obj;
+        }
+        if (rc != THETIS_OK) return rc;
+        if (ob.max_violation_eps <= target_eps || t + 1 == max_outer) break;
+        THETIS_TRY(alm_update(lp, ubar, zbar, beta));  // ubar -= beta r, zbar = z, then u^T a_j
+        if (ob.resid_inf > 0.5 * prev_res) beta = (float)((double)beta * (double)beta_growth);
+        prev_res = ob.resid_inf;
+    }
+    return THETIS_OK;
+}
+
 THETIS_API int thetis_objective(thetis_lp* lp, float beta, thetis_objective_t* out) {
     if (!lp || !out || !(beta > 0.0f)) return lp ? set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments") : THETIS_ERR_INVALID_ARG;
     return objective(lp, beta, out);

@@ -676,6 +676,20 @@ int recompute_r(thetis_lp* lp) {
     if (lp->d.m > 0) k_recompute_r<<<grid_for(lp->d.m, T), T, 0, lp->stream>>>(lp->d);
     return check_cuda(lp, "recompute_r");
 }
+// ALM anchor update (thetis_solve_alm): ubar_i -= beta r_i (fp32, product then
+// difference, each rounded), zbar_j = z_j
+__global__ void k_alm_update(DevLP L, float* __restrict__ ubar, float* __restrict__ zbar, float beta) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += stride)
+        ubar[i] = __fsub_rn(ubar[i], __fmul_rn(beta, L.r[i]));
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < L.N; j += stride) zbar[j] = L.z[j];
+}
+int alm_update(thetis_lp* lp, float* ubar, float* zbar, float beta) {
+    const int64_t n = lp->d.m > lp->d.N ? lp->d.m : lp->d.N;
+    if (n > 0) k_alm_update<<<grid_for(n, T), T, 0, lp->stream>>>(lp->d, ubar, zbar, beta);
+    THETIS_TRY(check_cuda(lp, "alm_update"));
+    return recompute_ua(lp);
+}
 int recompute_ua(thetis_lp* lp) {
     if (lp->d.n_s > 0) k_recompute_ua<<<grid_for(lp->d.n_s, T), T, 0, lp->stream>>>(lp->d);
     return check_cuda(lp, "recompute_ua");

@@ -221,6 +221,7 @@ int build_generic(thetis_lp* lp, int64_t m, int64_t n, int64_t nnz, const int64_
                   const float* lo, const float* hi, int obj_sense, int block_k, int64_t n_blocks);
 int recompute_r(thetis_lp* lp);
 int recompute_ua(thetis_lp* lp);
+int alm_update(thetis_lp* lp, float* ubar, float* zbar, float beta);  // ALM anchors (thetis_solve_alm)
 // colour.cu
 int ensure_colouring(thetis_lp* lp, uint64_t seed);
 // scd.cu
