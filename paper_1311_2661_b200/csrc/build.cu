@@ -416,17 +416,14 @@ __global__ void k_recompute_r(DevLP L) {
     }
 }
 // ua_j = ubar^T a_j, sequential over the column (same contract as the gradient dot)
+// ua_j = ubar^T a_j with the contract's column dot, one warp per column
 __global__ void k_recompute_ua(DevLP L) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < L.n_s; j += (int64_t)gridDim.x * blockDim.x) {
-        float acc = 0.0f;
-        if (L.ubar)
-            for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) {
-                int64_t row;
-                float a;
-                entry(L, t, row, a);
-                acc = __fadd_rn(acc, __fmul_rn(a, L.ubar[row]));
-            }
-        L.ua[j] = acc;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = w0; j < L.n_s; j += nw) {
+        const float acc = L.ubar ? col_dot_tree_warp(L, j, L.ubar, lane) : 0.0f;
+        if (lane == 0) L.ua[j] = acc;
     }
 }
 
@@ -691,7 +688,7 @@ int alm_update(thetis_lp* lp, float* ubar, float* zbar, float beta) {
     return recompute_ua(lp);
 }
 int recompute_ua(thetis_lp* lp) {
-    if (lp->d.n_s > 0) k_recompute_ua<<<grid_for(lp->d.n_s, T), T, 0, lp->stream>>>(lp->d);
+    if (lp->d.n_s > 0) k_recompute_ua<<<grid_for(32 * lp->d.n_s, T), T, 0, lp->stream>>>(lp->d);
     return check_cuda(lp, "recompute_ua");
 }
 

@@ -25,6 +25,9 @@
 // into kChunk pieces that any warp may claim: warps help finish pending heavy
 // tiles (FIFO in draw order) before drawing new positions.  The grid bounds the
 // number of workers to ~n_tiles / kAsyncDepth (bounded staleness).
+#include <algorithm>
+#include <array>
+
 #include <cub/cub.cuh>
 
 #include "thetis_internal.cuh"
@@ -33,7 +36,8 @@ namespace thetis {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int64_t kDetWarpCol = 64; // det: columns longer than this use the warp path
+constexpr int64_t kDetWarpCol = 32;  // det: columns longer than this use the warp path
+constexpr int64_t kDetCtaCol = 8192; // ... and longer than this a 1024-thread CTA (k_det_long)
 
 struct StepParams {
     float beta;       // caller's beta
@@ -83,19 +87,6 @@ __device__ __forceinline__ float clamp_lohi(float t, float lo, float hi) {
     return zn > hi ? hi : zn;
 }
 
-// sequential dot over column j in CSC order (the arithmetic contract)
-template <bool kAsync>
-__device__ __forceinline__ float col_dot_seq(const DevLP& L, int64_t j) {
-    float D = 0.0f;
-    for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) {
-        int64_t row;
-        float a;
-        entry(L, t, row, a);
-        float rv = kAsync ? ld_cg(L.r + row) : L.r[row];
-        D = __fadd_rn(D, L.val ? __fmul_rn(a, rv) : (a < 0.0f ? -rv : rv));
-    }
-    return D;
-}
 template <bool kAsync>
 __device__ __forceinline__ void col_scatter(const DevLP& L, int64_t j, float d) {
     if (d == 0.0f) return;
@@ -112,10 +103,10 @@ __device__ __forceinline__ void col_scatter(const DevLP& L, int64_t j, float d) 
 __device__ __forceinline__ float zbar_of(const DevLP& L, int64_t j) { return L.zbar ? L.zbar[j] : 0.0f; }
 __device__ __forceinline__ float ua_of(const DevLP& L, int64_t j) { return L.ubar ? L.ua[j] : 0.0f; }
 
-// scalar structural column, one thread
+// scalar structural column, one thread (the contract's column dot, thetis_internal.cuh)
 template <bool kAsync>
 __device__ __forceinline__ void update_scalar_seq(const DevLP& L, const StepParams& P, int64_t j) {
-    float D = col_dot_seq<kAsync>(L, j);
+    float D = col_dot_tree_thread(L, j, L.r);
     float z = L.z[j];
     float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
     float invL = unit_invL(P, col_norm2(L, j));
@@ -180,7 +171,7 @@ __device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParam
     for (int l = 0; l < KC; l++)
         if (l < k) {
             int64_t j = f + l;
-            float D = col_dot_seq<kAsync>(L, j);
+            float D = col_dot_tree_thread(L, j, L.r);
             float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
             y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
         }
@@ -228,57 +219,130 @@ __device__ __forceinline__ void update_slack(const DevLP& L, const StepParams& P
 template <int KC>
 __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const int32_t* __restrict__ members,
                                                    int64_t count) {
-    const int lane = threadIdx.x & 31;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t warp_base = idx - lane;
-    if (warp_base >= count) return;
-    int64_t u = idx < count ? (int64_t)members[idx] : -1;
-    bool deferred = false;
-    if (u >= 0) {
-        if (u < L.n_blocks) {
-            update_block_seq<false, KC>(L, P, u);
-        } else {
-            int64_t j = L.n_blocks * L.k + (u - L.n_blocks);
-            if (L.colptr[j + 1] - L.colptr[j] > kDetWarpCol) deferred = true;
-            else update_scalar_seq<false>(L, P, j);
+    if (idx >= count) return;
+    const int64_t u = members[idx];
+    if (u < L.n_blocks) {
+        update_block_seq<false, KC>(L, P, u);
+    } else {
+        const int64_t j = L.n_blocks * L.k + (u - L.n_blocks);
+        if (L.colptr[j + 1] - L.colptr[j] <= kDetWarpCol) update_scalar_seq<false>(L, P, j);
+        // longer columns: k_det_mid (one warp each) and k_det_long (one CTA each)
+    }
+}
+
+// det: one warp per scalar column with kDetWarpCol < nnz <= kDetCtaCol
+__global__ void __launch_bounds__(256) k_det_mid(DevLP L, StepParams P, const int32_t* __restrict__ cols, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const int64_t j = cols[w];
+    const int64_t beg = L.colptr[j], end = L.colptr[j + 1];
+    const float D = col_dot_tree_warp(L, j, L.r, lane);
+    float z = L.z[j];
+    float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
+    float invL = unit_invL(P, col_norm2(L, j));
+    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
+    float d = __fsub_rn(zn, z);
+    if (d != 0.0f)  // the column's rows are distinct: eight read-modify-writes in flight
+        for (int64_t t0 = beg + lane; t0 < end; t0 += 32 * 8) {
+            int64_t row[8];
+            float a[8], rv[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int64_t t = t0 + 32 * q;
+                row[q] = 0;
+                a[q] = 0.0f;
+                if (t < end) entry(L, t, row[q], a[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) rv[q] = t0 + 32 * q < end ? L.r[row[q]] : 0.0f;
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (t0 + 32 * q < end) {
+                    const float ad = L.val ? __fmul_rn(a[q], d) : (a[q] < 0.0f ? -d : d);
+                    L.r[row[q]] = __fadd_rn(rv[q], ad);
+                }
+        }
+    if (lane == 0) L.z[j] = zn;
+}
+
+// det: one 1024-thread CTA per scalar column longer than kDetCtaCol (power-law hubs):
+// thread l is the contract's virtual lane l, the halving goes through shared memory
+// (off >= 32) and warp 0's shuffles; the step on thread 0; then every thread scatters
+__global__ void __launch_bounds__(1024) k_det_long(DevLP L, StepParams P, const int32_t* __restrict__ cols) {
+    __shared__ float sp[1024];
+    __shared__ float s_d, s_zn;
+    constexpr int kU = 16;  // loads in flight per thread
+    const int l = threadIdx.x, lane = l & 31;
+    const int64_t j = cols[blockIdx.x];
+    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
+    float p = 0.0f;
+    for (int64_t t0 = cb + l; t0 < ce; t0 += kU * 1024) {
+        float x[kU];
+#pragma unroll
+        for (int q = 0; q < kU; q++) x[q] = t0 + 1024 * q < ce ? dot_term(L, t0 + 1024 * q, L.r) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < kU; q++)
+            if (t0 + 1024 * q < ce) p = __fadd_rn(p, x[q]);
+    }
+    sp[l] = p;
+    __syncthreads();
+    for (int off = 512; off >= 32; off >>= 1) {
+        if (l < off) sp[l] = __fadd_rn(sp[l], sp[l + off]);
+        __syncthreads();
+    }
+    if (l < 32) {
+        float q = sp[l];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const float o = __shfl_down_sync(0xffffffffu, q, off);
+            if (lane < off) q = __fadd_rn(q, o);
+        }
+        if (l == 0) {
+            const float z = L.z[j];
+            const float g = grad_from(c_int(L, j), ua_of(L, j), q, z, zbar_of(L, j), P.beta);
+            const float invL = unit_invL(P, col_norm2(L, j));
+            const float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
+            s_d = __fsub_rn(zn, z);
+            s_zn = zn;
         }
     }
-    unsigned pending = __ballot_sync(0xffffffffu, deferred);
-    while (pending) {
-        const int src = __ffs(pending) - 1;
-        pending &= pending - 1;
-        const int64_t us = __shfl_sync(0xffffffffu, u, src);
-        const int64_t j = L.n_blocks * L.k + (us - L.n_blocks);
-        const int64_t beg = L.colptr[j], end = L.colptr[j + 1];
-        float D = 0.0f;
-        for (int64_t base = beg; base < end; base += 32) {
-            int64_t t = base + lane;
-            float v = 0.0f;
-            if (t < end) {
-                int64_t row;
-                float a;
-                entry(L, t, row, a);
-                float rv = L.r[row];
-                v = L.val ? __fmul_rn(a, rv) : (a < 0.0f ? -rv : rv);
+    __syncthreads();
+    const float d = s_d;
+    if (d != 0.0f)
+        for (int64_t t0 = cb + l; t0 < ce; t0 += kU * 1024) {
+            int64_t row[kU];
+            float a[kU], rv[kU];
+#pragma unroll
+            for (int q = 0; q < kU; q++) {
+                row[q] = 0;
+                a[q] = 0.0f;
+                if (t0 + 1024 * q < ce) entry(L, t0 + 1024 * q, row[q], a[q]);
             }
-            const int lim = (int)((end - base) < 32 ? (end - base) : 32);
-            for (int q = 0; q < lim; q++) D = __fadd_rn(D, __shfl_sync(0xffffffffu, v, q));
+#pragma unroll
+            for (int q = 0; q < kU; q++) rv[q] = t0 + 1024 * q < ce ? L.r[row[q]] : 0.0f;
+#pragma unroll
+            for (int q = 0; q < kU; q++)
+                if (t0 + 1024 * q < ce) L.r[row[q]] = __fadd_rn(rv[q], L.val ? __fmul_rn(a[q], d) : (a[q] < 0.0f ? -d : d));
         }
-        float z = L.z[j];
-        float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
-        float invL = unit_invL(P, col_norm2(L, j));
-        float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-        float d = __fsub_rn(zn, z);
-        if (d != 0.0f)
-            for (int64_t t = beg + lane; t < end; t += 32) {
-                int64_t row;
-                float a;
-                entry(L, t, row, a);
-                float ad = L.val ? __fmul_rn(a, d) : (a < 0.0f ? -d : d);
-                L.r[row] = __fadd_rn(L.r[row], ad);
-            }
-        if (lane == 0) L.z[j] = zn;
-        __syncwarp();
+    if (l == 0) L.z[j] = s_zn;
+}
+// the class members' scalar columns longer than kDetWarpCol (unordered): (member
+// position, column, 1 if longer than kDetCtaCol)
+__global__ void k_det_long_list(DevLP L, int64_t S, const int32_t* __restrict__ members, int32_t* pos,
+                                unsigned long long* count) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < S; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = members[p];
+        if (u < L.n_blocks) continue;
+        const int64_t j = L.n_blocks * L.k + (u - L.n_blocks);
+        const int64_t len = L.colptr[j + 1] - L.colptr[j];
+        if (len > kDetWarpCol) {
+            const unsigned long long i = atomicAdd(count, 1ull);
+            pos[3 * i] = (int32_t)p;
+            pos[3 * i + 1] = (int32_t)j;
+            pos[3 * i + 2] = len > kDetCtaCol;
+        }
     }
 }
 
@@ -1200,7 +1264,48 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     P.rule = step_rule;
     const double Lmax = (double)beta * lp->maxnorm2 + 1.0 / (double)beta; // Eq. 7
     P.invLmax = (float)(1.0 / Lmax);
-    if (mode == THETIS_MODE_DETERMINISTIC) THETIS_TRY(ensure_colouring(lp, seed));
+    // det: the class members' scalar columns longer than kDetWarpCol, grouped by class
+    // (ascending member position): medium ones for k_det_mid, long ones for k_det_long
+    std::vector<int64_t> mid_ptr, long_ptr;
+    int32_t *mid_cols = nullptr, *long_cols = nullptr;
+    if (mode == THETIS_MODE_DETERMINISTIC) {
+        THETIS_TRY(ensure_colouring(lp, seed));
+        const int64_t S = L.n_blocks + L.n_scalar;
+        mid_ptr.assign(lp->K + 1, 0);
+        long_ptr.assign(lp->K + 1, 0);
+        if (S > 0 && L.nnz_s > kDetWarpCol) {
+            Carver C(lp->temp);
+            int32_t* pos = C.take<int32_t>(3 * S);
+            unsigned long long* cnt = C.take<unsigned long long>(1);
+            mid_cols = C.take<int32_t>(S);
+            long_cols = C.take<int32_t>(S);
+            if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "det long columns");
+            CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
+            const int64_t n_class = lp->class_ptr[lp->K];
+            if (n_class > 0) k_det_long_list<<<grid_for(n_class, 256), 256, 0, s>>>(L, n_class, lp->members, pos, cnt);
+            unsigned long long h = 0;
+            CUDA_TRY(lp, cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+            std::vector<std::array<int32_t, 3>> lst(h);
+            if (h) {
+                CUDA_TRY(lp, cudaMemcpyAsync(lst.data(), pos, h * 12, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(lp, cudaStreamSynchronize(s));
+            }
+            std::sort(lst.begin(), lst.end());
+            std::vector<int32_t> mc, lc;
+            size_t q = 0;
+            for (int64_t c = 0; c < lp->K; c++) {
+                mid_ptr[c] = (int64_t)mc.size();
+                long_ptr[c] = (int64_t)lc.size();
+                for (; q < lst.size() && lst[q][0] < lp->class_ptr[c + 1]; q++) (lst[q][2] ? lc : mc).push_back(lst[q][1]);
+            }
+            mid_ptr[lp->K] = (int64_t)mc.size();
+            long_ptr[lp->K] = (int64_t)lc.size();
+            if (!mc.empty()) CUDA_TRY(lp, cudaMemcpyAsync(mid_cols, mc.data(), mc.size() * 4, cudaMemcpyHostToDevice, s));
+            if (!lc.empty()) CUDA_TRY(lp, cudaMemcpyAsync(long_cols, lc.data(), lc.size() * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));  // `mc`, `lc` are pageable host memory
+        }
+    }
     const int64_t n_tiles = struct_tiles(L); // (3) permutes the tiles of structural units
     const bool serial = mode == THETIS_MODE_ASYNC_SERIAL;
     AsyncCtx AC{};
@@ -1339,6 +1444,9 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 int64_t beg = lp->class_ptr[c], cnt = lp->class_ptr[c + 1] - beg;
                 if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
                 else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
+                const int64_t nm = mid_ptr[c + 1] - mid_ptr[c], nl = long_ptr[c + 1] - long_ptr[c];
+                if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, s>>>(L, P, mid_cols + mid_ptr[c], nm);
+                if (nl > 0) k_det_long<<<(unsigned)nl, 1024, 0, s>>>(L, P, long_cols + long_ptr[c]);
             }
             if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, s>>>(L, P);
         } else {

@@ -94,6 +94,92 @@ __device__ __forceinline__ void entry(const DevLP& L, int64_t t, int64_t& row, f
     row = (int64_t)(raw & kRowMask);
     a = L.val ? L.val[t] : ((raw & kSignBit) ? -1.0f : 1.0f);
 }
+
+// ---- the column dot a_j^T v of the deterministic arithmetic contract (R-7,
+// SURVEY §8(c).4): virtual lane l in [0, 1024) sums the column's entries at positions
+// t = l, l + 1024, ... (CSC order) from +0, each product rounded on its own; then
+// p[l] += p[l + off] for l < off, off = 512, ..., 1; the dot is p[0].  Lanes past the
+// column hold +0 and adding +0 changes no lane value, so every evaluation below
+// skips them and gives the same bits.
+__device__ __forceinline__ float dot_term(const DevLP& L, int64_t t, const float* v) {
+    int64_t row;
+    float a;
+    entry(L, t, row, a);
+    const float x = v[row];
+    return L.val ? __fmul_rn(a, x) : (a < 0.0f ? -x : x);
+}
+// one thread, columns of at most W entries (registers)
+template <int W>
+__device__ __forceinline__ float col_dot_tree_small(const DevLP& L, int64_t cb, int64_t len, const float* v) {
+    float p[W];
+#pragma unroll
+    for (int i = 0; i < W; i++) p[i] = i < len ? __fadd_rn(0.0f, dot_term(L, cb + i, v)) : 0.0f;
+#pragma unroll
+    for (int s = W / 2; s >= 1; s >>= 1)
+#pragma unroll
+        for (int i = 0; i < s; i++) p[i] = __fadd_rn(p[i], p[i + s]);
+    return p[0];
+}
+__device__ __forceinline__ float col_dot_tree16(const DevLP& L, int64_t cb, int64_t len, const float* v) {
+    if (len <= 4) return col_dot_tree_small<4>(L, cb, len, v);
+    if (len <= 8) return col_dot_tree_small<8>(L, cb, len, v);
+    if (len <= 16) return col_dot_tree_small<16>(L, cb, len, v);
+    return col_dot_tree_small<32>(L, cb, len, v);
+}
+// one thread, any column: the lanes in the order the halving combines them (lane
+// bit-reversal), partial sums on a stack by level
+__device__ __forceinline__ float col_dot_tree_thread(const DevLP& L, int64_t j, const float* v) {
+    const int64_t cb = L.colptr[j], len = L.colptr[j + 1] - cb;
+    if (len <= 32) return col_dot_tree16(L, cb, len, v);
+    int lg = 0;
+    while ((1LL << lg) < len && lg < 10) lg++;
+    const int P = 1 << lg;
+    float st[12];
+    int lv[12], sp = 0;
+    for (int k = 0; k < P; k++) {
+        const int l = (int)(__brev((unsigned)k) >> (32 - lg));
+        float x = 0.0f;
+        for (int64_t t = l; t < len; t += 1024) x = __fadd_rn(x, dot_term(L, cb + t, v));
+        st[sp] = x;
+        lv[sp++] = 0;
+        while (sp >= 2 && lv[sp - 1] == lv[sp - 2]) {
+            st[sp - 2] = __fadd_rn(st[sp - 2], st[sp - 1]);
+            lv[sp - 2]++;
+            sp--;
+        }
+    }
+    return st[0];
+}
+// one warp, any column: lane q holds the virtual lanes q + 32 i, i < 32; returns the
+// dot on every lane
+__device__ __forceinline__ float col_dot_tree_warp(const DevLP& L, int64_t j, const float* v, int lane) {
+    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
+    float p[32];
+#pragma unroll
+    for (int i = 0; i < 32; i++) p[i] = 0.0f;
+    for (int64_t c0 = cb; c0 < ce; c0 += 1024) {
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int64_t t = c0 + lane + 32 * i;
+            x[i] = t < ce ? dot_term(L, t, v) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+            if (c0 + lane + 32 * i < ce) p[i] = __fadd_rn(p[i], x[i]);
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1)  // off = 512 .. 32: within the lane
+#pragma unroll
+        for (int i = 0; i < s; i++) p[i] = __fadd_rn(p[i], p[i + s]);
+    float q = p[0];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {  // off = 16 .. 1: across lanes
+        const float o = __shfl_down_sync(0xffffffffu, q, off);
+        if (lane < off) q = __fadd_rn(q, o);
+    }
+    return __shfl_sync(0xffffffffu, q, 0);
+}
 __device__ __forceinline__ double col_norm2(const DevLP& L, int64_t j) {
     return L.colnorm2 ? L.colnorm2[j] : (double)(L.colptr[j + 1] - L.colptr[j]);
 }

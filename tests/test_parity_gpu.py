@@ -167,9 +167,26 @@ def test_det_random_graphs(th, problem, rule):
     det_run(g, r32, r64, 10.0, 8, 5, rule)
 
 
+@pytest.mark.parametrize("problem", [VC, MIS])
+def test_det_long_columns_cta_path(th, problem):
+    # two stars (degrees 20000 and 9000) + a star of 1500 + random edges: columns above
+    # kDetCtaCol = 8192 go to the 1024-thread CTA path (k_det_long), 16 < nnz <= 8192 to
+    # the warp path; all follow the contract's 1024-lane halving (bit-exact)
+    rng = np.random.default_rng(4)
+    n = 30000
+    src = np.concatenate([np.zeros(20000, np.int32), np.full(9000, 1, np.int32), np.full(1500, 2, np.int32),
+                          rng.integers(3, n, 30000).astype(np.int32)])
+    dst = np.concatenate([rng.permutation(np.arange(3, n))[:20000].astype(np.int32),
+                          rng.permutation(np.arange(3, n))[:9000].astype(np.int32),
+                          rng.integers(3, n, 1500).astype(np.int32), rng.integers(3, n, 30000).astype(np.int32)])
+    vw = rng.uniform(1, 10, n).astype(np.float32)
+    g, r32, r64 = both(th, problem, n, src, dst, vw=vw)
+    det_run(g, r32, r64, 10.0, 4, 3, 1)
+
+
 def test_det_hub_column_warp_path(th):
-    # a star + random edges: the hub column (> 64 nnz) takes the warp-cooperative
-    # path with the same sequential summation order
+    # a star + random edges: the hub column (> 16 nnz) takes the warp-cooperative
+    # path with the contract's summation order
     rng = np.random.default_rng(0)
     src = np.concatenate([np.zeros(5000, np.int32), rng.integers(1, 4000, 8000).astype(np.int32)])
     dst = np.concatenate([np.arange(1, 5001, dtype=np.int32) % 4000, rng.integers(1, 4000, 8000).astype(np.int32)])
