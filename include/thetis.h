@@ -74,7 +74,9 @@ enum { THETIS_STEP_LMAX = 0, /* Alg. 1: 1/L_max, Eq. 7 */
 enum { THETIS_ROUND_VC_HALF = 1,   /* Lemma-1 threshold (1-eps)/2 + fix-up */
        THETIS_ROUND_VC_FIXUP = 2,  /* threshold 1/2 on raw x + fix-up */
        THETIS_ROUND_MIS_GREEDY = 3,/* packing alpha + greedy repair */
-       THETIS_ROUND_MWC_CKR = 4    /* CKR region growing, best of reps */ };
+       THETIS_ROUND_MWC_CKR = 4,   /* CKR region growing, best of reps */
+       THETIS_ROUND_SC_THRESHOLD = 5, /* set cover: x_s >= (1-eps)/f + fix-up (App. B.1; R-20) */
+       THETIS_ROUND_SC_RANDOM = 6     /* set cover: keep s w.p. min(1, d x_s) + fix-up (App. B.1; R-20) */ };
 
 #define THETIS_MAX_EPOCH_TIMES 64
 
@@ -234,7 +236,18 @@ THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float b
 /* ---- round ------------------------------------------------------------ */
 
 /* Round the current x.  out_assign (device or host, may be NULL): uint8[n]
- * vertex selection (VC/MIS) or label (MWC).  seed / reps: MWC_CKR only. */
+ * vertex selection (VC/MIS) or label (MWC); for the set-cover rules uint8[n_struct]
+ * set selection.  seed: MWC_CKR and SC_RANDOM; reps: MWC_CKR only.
+ * Set cover (NEXT-3, R-20): a generic LP whose rows all read sum_{s in row} x_s >= 1
+ * (GE, b = 1, coefficients 1; else THETIS_ERR_ROUND_PRECONDITION), columns = sets,
+ * rows = elements, f = the largest row count.  eps = max_rows (1 - sum x)_+ in fp32
+ * (sum in CSR order); SC_THRESHOLD selects x_s >= (1 - eps)/f (f-approximation of
+ * Hochbaum, on x/(1 - eps)), or 1/f with fallback = 1 when eps >= 1;
+ * SC_RANDOM keeps s iff u_s < min(1, d x_s), d = ceil(ln(2 m)), u_s counter-based
+ * (SplitMix64 of seed ^ 0x5851F42D4C957F2D (s + 1)), fallback = 1 when that sample
+ * left an element uncovered.  Both then add, for every uncovered element, its set
+ * with the largest x (ties: smaller cost, then smaller index), judged against the
+ * pre-fix-up selection; rounds = sets added, eps_or_alpha = eps. */
 THETIS_API int thetis_round(thetis_lp* lp, int rule, uint64_t seed, int reps, uint8_t* out_assign,
                             thetis_round_result* out /* host */);
 /* Same on an explicit structural point x float[n_struct] (host or device). */

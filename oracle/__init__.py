@@ -19,6 +19,7 @@ PROB_VC, PROB_MIS, PROB_MWC = 1, 2, 3
 MODE_DET, MODE_ASYNC, MODE_CYCLIC, MODE_TILE_SYNC = 0, 1, 2, 3
 STEP_LMAX, STEP_LJ = 0, 1
 ROUND_VC_HALF, ROUND_VC_FIXUP, ROUND_MIS_GREEDY, ROUND_MWC_CKR = 1, 2, 3, 4
+ROUND_SC_THRESHOLD, ROUND_SC_RANDOM = 5, 6
 SENSE_EQ, SENSE_GE, SENSE_LE = 0, 1, 2
 
 
@@ -264,21 +265,23 @@ class RefLP:
 
     def round_x(self, x, rule, seed=0, reps=10):
         x = _arr(x, np.float32)
-        out = np.zeros(max(self.n_vertices, 1), np.uint8)
+        n_out = self.n_struct if rule in (ROUND_SC_THRESHOLD, ROUND_SC_RANDOM) else self.n_vertices
+        out = np.zeros(max(n_out, 1), np.uint8)
         res = RefRound()
         rc = self._L.thetis_ref_round_x(self._h, x.ctypes.data, rule, seed, reps, out.ctypes.data,
                                         ctypes.byref(res))
         if rc != 0:
             raise OracleError(rc, "thetis_ref_round_x")
-        return out[: self.n_vertices], {f: getattr(res, f) for f, _ in RefRound._fields_}
+        return out[:n_out], {f: getattr(res, f) for f, _ in RefRound._fields_}
 
     def round(self, rule, seed=0, reps=10):
-        out = np.zeros(max(self.n_vertices, 1), np.uint8)
+        n_out = self.n_struct if rule in (ROUND_SC_THRESHOLD, ROUND_SC_RANDOM) else self.n_vertices
+        out = np.zeros(max(n_out, 1), np.uint8)
         res = RefRound()
         rc = self._L.thetis_ref_round(self._h, rule, seed, reps, out.ctypes.data, ctypes.byref(res))
         if rc != 0:
             raise OracleError(rc, "thetis_ref_round")
-        return out[: self.n_vertices], {f: getattr(res, f) for f, _ in RefRound._fields_}
+        return out[:n_out], {f: getattr(res, f) for f, _ in RefRound._fields_}
 
 
 def tile_perm(n_tiles, seed, epoch, bits=64):

@@ -26,7 +26,8 @@ enum { SENSE_EQ = 0, SENSE_GE = 1, SENSE_LE = 2 };
 enum { OBJ_MIN = 0, OBJ_MAX = 1 };
 enum { MODE_DET = 0, MODE_ASYNC = 1, MODE_CYCLIC = 2 };
 enum { STEP_LMAX = 0, STEP_LJ = 1 };
-enum { ROUND_VC_HALF = 1, ROUND_VC_FIXUP = 2, ROUND_MIS_GREEDY = 3, ROUND_MWC_CKR = 4 };
+enum { ROUND_VC_HALF = 1, ROUND_VC_FIXUP = 2, ROUND_MIS_GREEDY = 3, ROUND_MWC_CKR = 4, ROUND_SC_THRESHOLD = 5,
+       ROUND_SC_RANDOM = 6 };
 
 struct ref_lp {
     int problem;
@@ -1010,9 +1011,88 @@ static int cmp_mis(const void* a, const void* b) {
     return p->id < q->id ? -1 : (p->id > q->id);
 }
 
+/* set cover (App. B.1; R-20) on a generic covering LP, rows
+ * sum_{s in row} x_s >= 1, columns = sets: eps = max_rows (1 - sum x)_+ in fp32 (row sum
+ * in ascending set order); SC_THRESHOLD picks x_s >= (1 - eps)/f, f = the largest row
+ * count (Hochbaum's f-approximation "pick all sets with x_s > 1/f", on the
+ * feasible point x/(1 - eps); >= for the boundary, SPEC's reading), or 1/f with
+ * fallback when eps >= 1; SC_RANDOM keeps s iff u_s < min(1, d x_s), d = ceil(ln 2m)
+ * (Srinivasan's scheme, with the repetitions of SPEC's ledger folded into
+ * d), u_s = the first SplitMix64 output seeded seed ^ (0x5851F42D4C957F2D (s+1)) as
+ * ((h >> 40) + 1/2) 2^-24; fallback = 1 if that sample left an element uncovered.
+ * Both then add, for each uncovered element, its set with the largest x (ties:
+ * smaller cost, then smaller index), judged against the pre-fix-up selection. */
+static int round_set_cover(const ref_lp* lp, const float* x, int rule, uint64_t seed, uint8_t* out,
+                           ref_round_result* res) {
+    if (lp->problem != PROB_GENERIC || lp->n_blocks > 0 || lp->obj_sense != OBJ_MIN) return REF_NOT_SUPPORTED;
+    const int64_t ns = lp->n_s, m = lp->m;
+    for (int64_t i = 0; i < m; i++) {
+        if (lp->sense[i] != SENSE_GE || lp->b[i] != (REAL)1) return REF_ROUND_PRECONDITION;
+        for (int64_t t = lp->rowptr[i]; t < lp->rowptr[i + 1]; t++)
+            if (lp->rval[t] != (REAL)1) return REF_ROUND_PRECONDITION;
+    }
+    float eps = 0.0f;
+    int64_t f = 0;
+    for (int64_t i = 0; i < m; i++) {
+        float sum = 0.0f;
+        for (int64_t t = lp->rowptr[i]; t < lp->rowptr[i + 1]; t++) sum = sum + x[lp->rcol[t]];
+        float v = 1.0f - sum;
+        if (v > eps) eps = v;
+        if (lp->rowptr[i + 1] - lp->rowptr[i] > f) f = lp->rowptr[i + 1] - lp->rowptr[i];
+    }
+    res->eps_or_alpha = (double)eps;
+    if (rule == ROUND_SC_THRESHOLD) {
+        float tau = f > 0 ? 1.0f / (float)f : 1.0f;
+        if (eps < 1.0f) tau = (1.0f - eps) / (float)f;
+        else res->fallback = 1;
+        for (int64_t s = 0; s < ns; s++) out[s] = x[s] >= tau ? 1 : 0;
+    } else {
+        const float d = (float)ceil(log(2.0 * (double)(m > 0 ? m : 1)));
+        for (int64_t s = 0; s < ns; s++) {
+            float p = d * x[s];
+            if (p > 1.0f) p = 1.0f;
+            uint64_t h = sm64_out(seed ^ (0x5851F42D4C957F2DULL * (uint64_t)(s + 1)), 0);
+            float u = ((float)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+            out[s] = u < p ? 1 : 0;
+        }
+    }
+    uint8_t* add = (uint8_t*)xcalloc(ns + 1, 1);
+    int64_t uncovered = 0;
+    for (int64_t i = 0; i < m; i++) {
+        const int64_t a = lp->rowptr[i], b = lp->rowptr[i + 1];
+        int covered = 0;
+        for (int64_t t = a; t < b; t++) if (out[lp->rcol[t]]) covered = 1;
+        if (covered || a == b) continue;
+        uncovered++;
+        int32_t pick = lp->rcol[a];
+        for (int64_t t = a + 1; t < b; t++) {
+            int32_t s = lp->rcol[t];
+            if (x[s] > x[pick] || (x[s] == x[pick] && (lp->c_orig[s] < lp->c_orig[pick] ||
+                                                       (lp->c_orig[s] == lp->c_orig[pick] && s < pick))))
+                pick = s;
+        }
+        add[pick] = 1;
+    }
+    if (rule == ROUND_SC_RANDOM) res->fallback = uncovered > 0;
+    for (int64_t s = 0; s < ns; s++) if (add[s] && !out[s]) { out[s] = 1; res->rounds++; }
+    free(add);
+    double cost = 0.0;
+    int64_t sel = 0;
+    for (int64_t s = 0; s < ns; s++) if (out[s]) { cost += (double)lp->c_orig[s]; sel++; }
+    int64_t feas = 1;
+    for (int64_t i = 0; i < m; i++) {
+        int covered = 0;
+        for (int64_t t = lp->rowptr[i]; t < lp->rowptr[i + 1]; t++) if (out[lp->rcol[t]]) covered = 1;
+        if (!covered) feas = 0;
+    }
+    res->cost = cost; res->n_selected = sel; res->feasible = feas;
+    return REF_OK;
+}
+
 int thetis_ref_round_x(const ref_lp* lp, const float* x, int rule, uint64_t seed, int reps,
                        uint8_t* out, ref_round_result* res) {
     memset(res, 0, sizeof(*res));
+    if (rule == ROUND_SC_THRESHOLD || rule == ROUND_SC_RANDOM) return round_set_cover(lp, x, rule, seed, out, res);
     int64_t n = lp->n_vert, me = lp->m_edges;
     if (rule == ROUND_VC_HALF || rule == ROUND_VC_FIXUP) {
         if (lp->problem != PROB_VC) return REF_NOT_SUPPORTED;

@@ -36,6 +36,7 @@ THETIS_PROB_GENERIC, THETIS_PROB_VC, THETIS_PROB_MIS, THETIS_PROB_MWC = 0, 1, 2,
 THETIS_MODE_DETERMINISTIC, THETIS_MODE_ASYNC, THETIS_MODE_ASYNC_SERIAL = 0, 1, 2
 THETIS_STEP_LMAX, THETIS_STEP_LJ = 0, 1
 THETIS_ROUND_VC_HALF, THETIS_ROUND_VC_FIXUP, THETIS_ROUND_MIS_GREEDY, THETIS_ROUND_MWC_CKR = 1, 2, 3, 4
+THETIS_ROUND_SC_THRESHOLD, THETIS_ROUND_SC_RANDOM = 5, 6
 THETIS_MAX_EPOCH_TIMES = 64
 
 LIB_PATH = _LIB_PATH
@@ -303,15 +304,16 @@ class LP:
     def _round(self, x, rule, seed, reps, out):
         res = RoundResult()
         torch = _torch()
+        n_out = self.n_struct if rule in (THETIS_ROUND_SC_THRESHOLD, THETIS_ROUND_SC_RANDOM) else self.n_vertices
         if out is None:
-            out = torch.empty(max(self.n_vertices, 1), dtype=torch.uint8, device=self.device)
+            out = torch.empty(max(n_out, 1), dtype=torch.uint8, device=self.device)
         if x is None:
             rc = thetis_round(self._h, rule, seed, reps, out.data_ptr(), ctypes.byref(res))
         else:
             xt = _dev_array(x, torch.float32, self.device)
             rc = thetis_round_x(self._h, xt.data_ptr(), rule, seed, reps, out.data_ptr(), ctypes.byref(res))
         _check(rc, "thetis_round", self._h)
-        return out[: self.n_vertices], {f: getattr(res, f) for f, _ in RoundResult._fields_}
+        return out[:n_out], {f: getattr(res, f) for f, _ in RoundResult._fields_}
 
     def round(self, rule, seed=0, reps=10, out=None):
         return self._round(None, rule, seed, reps, out)

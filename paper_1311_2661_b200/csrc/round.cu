@@ -114,6 +114,87 @@ __global__ void k_sum_partials(int blocks, int width, const double* partial, dou
     out[q] = acc;
 }
 
+// ---------------- set cover (generic covering LP: rows sum_{s in row} x_s >= 1)
+// precondition, eps = max_rows (1 - sum x)_+ (fp32, CSR order) and f = max row count
+__global__ void __launch_bounds__(T) k_sc_rows(const DevLP L, const float* __restrict__ x, float* eps, int32_t* f,
+                                               int32_t* bad) {
+    float best = 0.0f;
+    int fm = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (L.sense[i] != THETIS_GE || L.b[i] != 1.0f) atomicOr(bad, 1);
+        float sum = 0.0f;
+        for (int64_t t = L.rowptr[i]; t < L.rowptr[i + 1]; t++) {
+            if (L.rval && L.rval[t] != 1.0f) atomicOr(bad, 1);
+            sum = __fadd_rn(sum, x[L.rcol[t]]);
+        }
+        best = fmaxf(best, __fsub_rn(1.0f, sum));
+        const int cnt = (int)(L.rowptr[i + 1] - L.rowptr[i]);
+        fm = cnt > fm ? cnt : fm;
+    }
+    for (int o = 16; o; o >>= 1) fm = max(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+    if ((threadIdx.x & 31) == 0 && fm) atomicMax(f, fm);
+    block_max_nonneg(eps, best);
+}
+__device__ __forceinline__ float sc_uniform(uint64_t seed, int64_t s) {
+    uint64_t z = seed ^ (0x5851F42D4C957F2DULL * (uint64_t)(s + 1));
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return ((float)(z >> 40) + 0.5f) * (1.0f / 16777216.0f);  // exact: 24-bit integer + 1/2, times 2^-24
+}
+__global__ void k_sc_select(int64_t n, int rule, const float* __restrict__ x, const float* eps_p, const int32_t* f_p,
+                            float d, uint64_t seed, uint8_t* sel, uint8_t* add, int32_t* fallback) {
+    const float eps = *eps_p;
+    const float f = (float)*f_p;
+    float tau = f > 0.0f ? __fdiv_rn(1.0f, f) : 1.0f;
+    if (rule == THETIS_ROUND_SC_THRESHOLD) {
+        if (eps < 1.0f) tau = __fdiv_rn(__fsub_rn(1.0f, eps), f);
+        else if (blockIdx.x == 0 && threadIdx.x == 0) *fallback = 1;
+    }
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        if (rule == THETIS_ROUND_SC_THRESHOLD) {
+            sel[s] = x[s] >= tau ? 1 : 0;
+        } else {
+            const float p = fminf(1.0f, __fmul_rn(d, x[s]));
+            sel[s] = sc_uniform(seed, s) < p ? 1 : 0;
+        }
+        add[s] = 0;
+    }
+}
+// every element without a selected set adds its set with the largest x (ties: smaller
+// cost, then smaller index); counts the uncovered elements
+__global__ void k_sc_fixup(const DevLP L, const float* __restrict__ x, const uint8_t* __restrict__ sel, uint8_t* add,
+                           unsigned long long* uncovered) {
+    unsigned long long u = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = L.rowptr[i], b = L.rowptr[i + 1];
+        bool covered = false;
+        for (int64_t t = a; t < b && !covered; t++) covered = sel[L.rcol[t]];
+        if (covered || a == b) continue;
+        u++;
+        int32_t pick = L.rcol[a];
+        for (int64_t t = a + 1; t < b; t++) {
+            const int32_t s = L.rcol[t];
+            const float xs = x[s], xp = x[pick];
+            if (xs > xp || (xs == xp && (L.c[s] < L.c[pick] || (L.c[s] == L.c[pick] && s < pick)))) pick = s;
+        }
+        add[pick] = 1;
+    }
+    for (int o = 16; o; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+    if ((threadIdx.x & 31) == 0 && u) atomicAdd(uncovered, u);
+}
+__global__ void k_sc_bad_rows(const DevLP L, const uint8_t* __restrict__ sel, unsigned long long* bad) {
+    unsigned long long b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        bool covered = false;
+        for (int64_t t = L.rowptr[i]; t < L.rowptr[i + 1] && !covered; t++) covered = sel[L.rcol[t]];
+        b += !covered;
+    }
+    for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
+}
+
 // ---------------- MIS
 __global__ void k_mis_alpha(int64_t m, const int2* __restrict__ edges, const float* __restrict__ x, float* alpha) {
     float best = 0.0f;
@@ -238,7 +319,8 @@ int round_x(thetis_lp* lp, const float* x, int rule, uint64_t seed, int reps, ui
     const DevLP& L = lp->d;
     cudaStream_t s = lp->stream;
     memset(res, 0, sizeof(*res));
-    const int64_t n = L.n_vert, m = L.m_edges;
+    const bool sc = rule == THETIS_ROUND_SC_THRESHOLD || rule == THETIS_ROUND_SC_RANDOM;
+    const int64_t n = sc ? L.n_s : L.n_vert, m = L.m_edges;
     Carver C(lp->temp);
     C.take<float>(L.n_s); // staging of a host x (see thetis_round_x)
     uint8_t* sel = C.take<uint8_t>(n);
@@ -357,6 +439,39 @@ int round_x(thetis_lp* lp, const float* x, int rule, uint64_t seed, int reps, ui
         res->best_rep = best;
         res->feasible = 1;
         res->n_selected = (int64_t)cut;
+    } else if (sc) {
+        if (L.problem != THETIS_PROB_GENERIC || L.n_blocks > 0 || L.obj_sense != THETIS_MIN)
+            return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "set-cover rounding needs a generic covering LP");
+        float* eps = (float*)small;
+        int32_t* f = small + 2;
+        int32_t* bad_in = small + 3;
+        const int gr = grid_for(L.m, T);
+        if (L.m > 0) k_sc_rows<<<gr, T, 0, s>>>(L, x, eps, f, bad_in);
+        int32_t hb = 0;
+        CUDA_TRY(lp, cudaMemcpyAsync(&hb, bad_in, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        if (hb) return set_error(lp, THETIS_ERR_ROUND_PRECONDITION, "set-cover rounding: a row is not sum x >= 1");
+        const float d = (float)ceil(log(2.0 * (double)(L.m > 0 ? L.m : 1)));
+        if (n > 0) k_sc_select<<<gv, T, 0, s>>>(n, rule, x, eps, f, d, seed, selp, add, small + 1);
+        if (L.m > 0) k_sc_fixup<<<gr, T, 0, s>>>(L, x, selp, add, cnt + 1);
+        k_vc_merge<<<kRedBlocks, T, 0, s>>>(n, L.c, selp, add, partial);
+        k_sum_partials<<<1, 32, 0, s>>>(kRedBlocks, 3, partial, sums);
+        if (L.m > 0) k_sc_bad_rows<<<gr, T, 0, s>>>(L, selp, cnt);
+        double h[3];
+        float he;
+        int32_t fb;
+        unsigned long long bad[2];
+        CUDA_TRY(lp, cudaMemcpyAsync(h, sums, 24, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaMemcpyAsync(&he, eps, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaMemcpyAsync(&fb, small + 1, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaMemcpyAsync(bad, cnt, 16, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        res->cost = h[0];
+        res->n_selected = (int64_t)h[1];
+        res->rounds = (int64_t)h[2];
+        res->eps_or_alpha = he;
+        res->fallback = rule == THETIS_ROUND_SC_THRESHOLD ? fb : (bad[1] > 0);
+        res->feasible = bad[0] == 0;
     } else {
         return set_error(lp, THETIS_ERR_INVALID_ARG, "unknown rounding rule %d", rule);
     }

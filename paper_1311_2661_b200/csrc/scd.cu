@@ -685,7 +685,6 @@ __global__ void k_pass_keys(DevLP L, HubCtx H, const uint8_t* __restrict__ range
 // the min side of D there, flushed with one atomic per hub column at the end.
 // kAnchor: the LP has anchors (zbar / ubar), else both are zero.  The slack step
 // is slack_new<true> written out for graph rows (sigma = sg for every row).
-constexpr int kPassRows = 4;
 // shared memory: d of the range (float) and the min side of D in fixed point with
 // resolution 2^-22, kept as two integer sums so that every addition is one native
 // shared atomic without a carry (a float add is a CAS loop): x 2^22 = h 2^12 + l with

@@ -1,0 +1,171 @@
+"""Set cover (App. B.1; R-20): the covering LP
+min c^T x s.t. sum_{s ∋ a} x_s >= 1, x in [0, 1], through the generic builder, and its two
+roundings (f-threshold and randomized, each with the element fix-up).
+
+Oracle pins (-m "not gpu"): SPEC's boundary examples; on edge-incidence systems (f = 2) the
+threshold rule is the vertex-cover rule; after the ALM outer loop (R-19) reaches the LP
+optimum (HiGHS) the threshold cover costs between IP* (brute force) and f LP*; the randomized
+rule keeps x_s = 1 sets always, and over many seeds keeps a set with frequency min(1, d x_s).
+GPU parity (-m gpu, C ABI): both rules bit-exact by cross-application with the oracle.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import RefLP
+
+scipy_opt = pytest.importorskip("scipy.optimize")
+
+TH, RND = oracle.ROUND_SC_THRESHOLD, oracle.ROUND_SC_RANDOM
+
+
+def set_system(n_sets, n_elem, seed, mean_extra=2.0):
+    """each element lies in 1 + Poisson(mean_extra) distinct random sets (at most n_sets)"""
+    rng = np.random.default_rng(seed)
+    members = []
+    for _ in range(n_elem):
+        k = min(n_sets, 1 + rng.poisson(mean_extra))
+        members.append(sorted(rng.choice(n_sets, size=k, replace=False).tolist()))
+    cost = (1.0 + rng.integers(0, 9, n_sets)).astype(np.float32)
+    return members, cost
+
+
+def covering_lp_arrays(n_sets, members):
+    """CSC (sets = columns) and CSR (elements = rows, ascending sets) of the covering rows"""
+    cols = [[] for _ in range(n_sets)]
+    for a, ss in enumerate(members):
+        for s in ss:
+            cols[s].append(a)
+    colptr = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+    rowidx = np.array([a for c in cols for a in c], np.int32)
+    rowptr = np.concatenate([[0], np.cumsum([len(ss) for ss in members])]).astype(np.int64)
+    colidx = np.array([s for ss in members for s in ss], np.int32)
+    return colptr, rowidx, rowptr, colidx
+
+
+def ref_cover_lp(n_sets, members, cost, bits=64, b=1.0):
+    m = len(members)
+    colptr, rowidx, _, _ = covering_lp_arrays(n_sets, members)
+    return RefLP.generic(m, n_sets, colptr, rowidx, np.ones(len(rowidx), np.float32), np.full(m, b, np.float32),
+                         cost, sense=np.full(m, oracle.SENSE_GE, np.int8), bits=bits)
+
+
+def covers(members, sel):
+    return all(any(sel[s] for s in ss) for ss in members)
+
+
+def test_spec_boundary_examples():
+    # one element in three sets at x = 1/3 each, f = 3: all three are picked
+    lp = ref_cover_lp(3, [[0, 1, 2]], np.ones(3, np.float32))
+    sel, res = lp.round_x(np.full(3, 1 / 3, np.float32), TH)
+    assert sel.tolist() == [1, 1, 1] and res["feasible"] == 1 and res["rounds"] == 0
+    # integral input is kept as is; x = 0 everywhere: threshold 1/f misses, the fix-up covers
+    members = [[0, 1], [1, 2], [2, 3]]
+    lp = ref_cover_lp(4, members, np.array([1, 2, 3, 4], np.float32))
+    sel, res = lp.round_x(np.array([1, 0, 1, 0], np.float32), TH)
+    assert sel.tolist() == [1, 0, 1, 0] and res["cost"] == 4.0
+    sel, res = lp.round_x(np.zeros(4, np.float32), TH)
+    assert res["fallback"] == 1 and res["feasible"] == 1 and covers(members, sel)
+    # ties in the fix-up: smaller cost, then smaller index
+    assert sel.tolist() == [1, 1, 1, 0]
+
+
+def test_f2_edge_incidence_is_the_vertex_cover_rule():
+    rng = np.random.default_rng(5)
+    n = 40
+    src, dst = rng.integers(0, n, 90).astype(np.int32), rng.integers(0, n, 90).astype(np.int32)
+    w = rng.uniform(1, 10, n).astype(np.float32)
+    g = RefLP.graph(1, n, src, dst, vertex_w=w)
+    eu, ev = g.edges()
+    members = [sorted((int(u), int(v))) for u, v in zip(eu, ev)]
+    sc = ref_cover_lp(n, members, w)
+    for trial in range(5):
+        x = rng.uniform(0, 1, n).astype(np.float32) * (0.6 + 0.2 * trial)
+        sv, rv = g.round_x(x, oracle.ROUND_VC_HALF)
+        ss, rs = sc.round_x(x, TH)
+        assert np.array_equal(sv, ss) and rv["cost"] == rs["cost"] and rv["eps_or_alpha"] == rs["eps_or_alpha"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_threshold_cover_between_ip_and_f_lp(seed):
+    n_sets, n_elem = 9, 12
+    members, cost = set_system(n_sets, n_elem, seed)
+    f = max(len(ss) for ss in members)
+    A = np.zeros((n_elem, n_sets))
+    for a, ss in enumerate(members):
+        A[a, ss] = 1.0
+    lp_res = scipy_opt.linprog(cost.astype(np.float64), A_ub=-A, b_ub=-np.ones(n_elem), bounds=[(0, 1)] * n_sets,
+                               method="highs")
+    lp_opt = lp_res.fun
+    ip_opt = min(float(cost[list(S)].sum()) for k in range(n_sets + 1) for S in itertools.combinations(range(n_sets), k)
+                 if all(any(s in S for s in ss) for ss in members))
+    lp = ref_cover_lp(n_sets, members, cost)
+    st = lp.solve_alm(10.0, 1.0, 15, 300, mode=oracle.MODE_DET, seed=seed, target_eps=-1.0)
+    assert st["lp_obj"][-1] == pytest.approx(lp_opt, rel=1e-4, abs=1e-4)
+    sel, res = lp.round(TH)
+    assert res["feasible"] == 1 and covers(members, sel)
+    assert ip_opt - 1e-9 <= res["cost"] <= f * lp_opt / (1.0 - res["eps_or_alpha"]) + 1e-6
+
+
+def test_randomized_rule():
+    members, cost = set_system(30, 60, 8)
+    lp = ref_cover_lp(30, members, cost)
+    x = np.zeros(30, np.float32)
+    x[[3, 7]] = 1.0
+    x[[1, 2, 5]] = [0.02, 0.05, 0.1]
+    d = np.ceil(np.log(2 * 60))
+    keep = np.zeros(30)
+    for sd in range(3000):
+        sel, res = lp.round_x(x, RND, seed=sd)
+        assert res["feasible"] == 1 and covers(members, sel)
+        raw = sel.copy()
+        keep += raw  # includes fix-up additions; only sets never added by the fix-up are checked below
+    assert keep[3] == keep[7] == 3000
+    # sets 1, 2, 5 are never the fix-up's pick when some x_s = 1 set covers their elements; check one
+    # that lies in no element covered by sets 3, 7 only through the raw probability
+    p = np.minimum(1.0, d * x)
+    for s in (1, 2, 5):
+        lo = 3000 * p[s] - 5 * np.sqrt(3000 * p[s] * (1 - p[s]))
+        assert keep[s] >= lo
+    sel, res = lp.round_x(np.zeros(30, np.float32), RND, seed=1)
+    assert res["fallback"] == 1 and res["feasible"] == 1 and res["n_selected"] == res["rounds"]
+
+
+def test_precondition():
+    lp = ref_cover_lp(3, [[0, 1], [1, 2]], np.ones(3, np.float32), b=2.0)
+    with pytest.raises(oracle.OracleError) as e:
+        lp.round_x(np.ones(3, np.float32), TH)
+    assert e.value.code == -6
+
+
+# ---------------------------------------------------------------- GPU parity
+@pytest.mark.gpu
+def test_set_cover_rounding_cross_application():
+    import paper_1311_2661_b200 as th
+    n_sets, n_elem = 3000, 20000
+    members, cost = set_system(n_sets, n_elem, 11, mean_extra=3.0)
+    colptr, rowidx, rowptr, colidx = covering_lp_arrays(n_sets, members)
+    ones = np.ones(len(rowidx), np.float32)
+    g = th.LP.from_csc_csr(n_elem, n_sets, colptr, rowidx, ones, rowptr, colidx, ones, np.ones(n_elem, np.float32),
+                           cost, sense=np.full(n_elem, th.THETIS_GE, np.int8))
+    r32 = ref_cover_lp(n_sets, members, cost, bits=32)
+    g.solve(10.0, 30, mode=th.THETIS_MODE_DETERMINISTIC, seed=3)
+    r32.solve(10.0, 30, mode=oracle.MODE_DET, seed=3)
+    assert np.array_equal(g.get_x().cpu().numpy(), r32.x32())
+    rng = np.random.default_rng(2)
+    xs = [r32.x32()[:n_sets], rng.uniform(0, 0.6, n_sets).astype(np.float32), np.zeros(n_sets, np.float32)]
+    for x in xs:
+        for rule, seed in ((th.THETIS_ROUND_SC_THRESHOLD, 0), (th.THETIS_ROUND_SC_RANDOM, 1),
+                           (th.THETIS_ROUND_SC_RANDOM, 99)):
+            sel, res = g.round_x(x, rule, seed=seed)
+            rsel, rres = r32.round_x(x, rule, seed=seed)
+            assert np.array_equal(sel.cpu().numpy(), rsel)
+            assert res["feasible"] == rres["feasible"] == 1
+            for k in ("cost", "eps_or_alpha", "fallback", "rounds", "n_selected"):
+                assert res[k] == rres[k], k
+    bad = th.LP.from_csc_csr(n_elem, n_sets, colptr, rowidx, ones, rowptr, colidx, ones,
+                             np.full(n_elem, 2.0, np.float32), cost, sense=np.full(n_elem, th.THETIS_GE, np.int8))
+    with pytest.raises(th.ThetisError):
+        bad.round_x(xs[1], th.THETIS_ROUND_SC_THRESHOLD)

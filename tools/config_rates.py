@@ -21,8 +21,26 @@ RUNS = [  # (config, mode, epochs cap)
     ("vc_chunglu_10m", 0, 3), ("vc_chunglu_10m", 1, None),
     ("mwc_grid_2048", 0, None), ("mwc_grid_2048", 1, None),
     ("vc_rmat_26", 1, None),
+    ("sc_1m", 0, None), ("sc_1m", 1, None),  # NEXT-3 set cover (not a BASELINE config)
 ]
-PROBLEM = {"vc_er_1k": 1, "mis_er_1m": 2, "vc_chunglu_10m": 1, "mwc_grid_2048": 3, "vc_rmat_26": 1}
+PROBLEM = {"vc_er_1k": 1, "mis_er_1m": 2, "vc_chunglu_10m": 1, "mwc_grid_2048": 3, "vc_rmat_26": 1, "sc_1m": 0}
+
+
+def set_cover_instance(n_elem=1_000_000, n_sets=200_000, mean_extra=4.0, seed=31):
+    """synthetic set cover (NEXT-3): element a lies in 1 + Poisson(mean_extra) random sets
+    (duplicates dropped); costs U[1, 10).  Returns the covering LP's CSC and CSR."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    k = 1 + rng.poisson(mean_extra, n_elem)
+    elem = np.repeat(np.arange(n_elem, dtype=np.int64), k)
+    sets = rng.integers(0, n_sets, len(elem))
+    key = np.unique(elem * n_sets + sets)
+    elem, sets = key // n_sets, key % n_sets
+    rowptr = np.concatenate([[0], np.cumsum(np.bincount(elem, minlength=n_elem))]).astype(np.int64)
+    order = np.lexsort((elem, sets))
+    colptr = np.concatenate([[0], np.cumsum(np.bincount(sets, minlength=n_sets))]).astype(np.int64)
+    cost = (1.0 + 9.0 * rng.random(n_sets)).astype(np.float32)
+    return (n_elem, n_sets, colptr, elem[order].astype(np.int32), rowptr, sets.astype(np.int32), cost)
 
 
 def main():
@@ -42,9 +60,20 @@ def main():
     for name, mode, cap in RUNS:
         if a.only and a.only not in name:
             continue
-        cfg = inputs.CONFIGS[name]
         prob = PROBLEM[name]
-        if name == "vc_rmat_26":
+        if name == "sc_1m":
+            import numpy as np
+            m_, n_, cp, ri, rp, ci, cost = cache.get(name) or set_cover_instance()
+            cache = {name: (m_, n_, cp, ri, rp, ci, cost)}
+            ones = np.ones(len(ri), np.float32)
+            lp = th.LP.from_csc_csr(m_, n_, cp, ri, ones, rp, ci, ones, np.ones(m_, np.float32), cost,
+                                    sense=np.full(m_, th.THETIS_GE, np.int8), device=dev)
+            cfg = type("C", (), dict(beta=10.0, epochs=30, solve_seed=7))
+        else:
+            cfg = inputs.CONFIGS[name]
+        if name == "sc_1m":
+            pass
+        elif name == "vc_rmat_26":
             p = cfg.params
             n, E = 1 << p["scale"], p["samples"]
             src = torch.empty(E, dtype=torch.int32, device=dev)
@@ -71,13 +100,21 @@ def main():
         nnz = st["nnz_processed"] / max(st["epochs"], 1)
         alg = 20 * lp.n_struct + 12 * lp.nnz_struct + 16 * lp.n_ineq
         ob = lp.objective(cfg.beta)
+        extra = {}
+        if name == "sc_1m":
+            import time
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, rr = lp.round(th.THETIS_ROUND_SC_THRESHOLD)
+            extra = dict(round_ms=(time.perf_counter() - t0) * 1e3, cover_cost=rr["cost"], feasible=rr["feasible"],
+                         lp_obj=ob["lp_obj"], eps=ob["max_violation_eps"])
         out = dict(config=name, mode="det" if mode == 0 else "async", epochs=epochs, ms_epoch_median=med,
                    ms_epoch_first=ms[0], updates_per_s=upd / med * 1e3, nnz_per_s=nnz / med * 1e3,
                    alg_bytes_per_epoch=alg, alg_GBps=alg / med / 1e6, frac_of_measured_hbm=alg / med / 1e6 / peak,
                    colours=st["n_colours"], n_struct=lp.n_struct, m=lp.m, nnz_struct=lp.nnz_struct,
                    f_beta=ob["f_beta"], drift_inf=ob["drift_inf"],
                    ms_row_pass=st["ms_row_pass"] / max(st["row_pass_launches"], 1),
-                   ms_hub_update=st["ms_hub_update"] / epochs, ms_tiles=st["ms_tiles"] / epochs)
+                   ms_hub_update=st["ms_hub_update"] / epochs, ms_tiles=st["ms_tiles"] / epochs, **extra)
         print(json.dumps(out), flush=True)
         del lp
         torch.cuda.empty_cache()
