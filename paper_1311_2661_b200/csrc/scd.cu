@@ -1173,10 +1173,13 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 }
 
 // Bounded staleness (the async scheme needs the number of concurrent
-// updaters small relative to n): at most ~n_tiles / kAsyncDepth warps work at
-// once (< 0.8% of the tiles), and never more than the device holds (persistent
-// grid); large LPs are bounded by the device, not by the depth.
-constexpr int64_t kAsyncDepth = 128;
+// updaters small relative to n): at most ~n_tiles / depth warps work at once, and
+// never more than the device holds (persistent grid); large LPs are bounded by the
+// device, not by the depth.  The bound "depends on n and on the diagonal dominance properties of the
+// Hessian": scalar columns (VC / MIS / generic) work with up to n_tiles / 32 tiles in
+// flight, the coupled simplex blocks of MWC with n_tiles / 128 (at n_tiles / 32 the
+// reduced config-4 run leaves the async tolerance; measured)
+constexpr int64_t kAsyncDepth = 32, kAsyncDepthBlocks = 128;
 static int64_t async_workers(int64_t n_tiles, int path) {
     static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
     if (!per_sm[path]) {
@@ -1191,7 +1194,7 @@ static int64_t async_workers(int64_t n_tiles, int path) {
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathLight>, kWarpsPerBlock * 32, 0);
         if (per_sm[path] < 1) per_sm[path] = 1;
     }
-    int64_t depth_cap = n_tiles / kAsyncDepth;
+    int64_t depth_cap = n_tiles / (path == kPathBlocks || path == kPathBlocks8 ? kAsyncDepthBlocks : kAsyncDepth);
     int64_t dev_cap = (int64_t)per_sm[path] * sms * kWarpsPerBlock;
     int64_t w = depth_cap < dev_cap ? depth_cap : dev_cap;
     return w < 1 ? 1 : w;
