@@ -137,3 +137,25 @@ def test_alm_validation(th):
     st, _, _ = g.solve_alm(10.0, 2.0, 3, 10, target_eps=1e9)
     assert st["rounds"] == 1
     del ctypes
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem", [VC, MIS])
+def test_alm_async_serial_with_hub_step_matches_replay(th, problem):
+    # anchors through the whole async epoch (row pass with anchors, hub step, light tiles
+    # through lv): the one-tile-in-flight kernel equals the oracle's tile-synchronous replay
+    rng = np.random.default_rng(2)
+    n = 20000
+    src = np.concatenate([rng.integers(0, 64, 60000), rng.integers(0, n, 40000)]).astype(np.int32)
+    dst = np.concatenate([rng.integers(0, n, 60000), rng.integers(0, n, 40000)]).astype(np.int32)
+    w = rng.uniform(1, 10, n).astype(np.float32)
+    g = th.LP.from_graph(problem, n, src, dst, vertex_w=w)
+    r = RefLP.graph(problem, n, src, dst, vertex_w=w)
+    st, ub, zb = g.solve_alm(10.0, 2.0, 3, 6, mode=th.THETIS_MODE_ASYNC_SERIAL, seed=5, target_eps=-1.0)
+    rs = r.solve_alm(10.0, 2.0, 3, 6, mode=oracle.MODE_TILE_SYNC, seed=5, target_eps=-1.0)
+    assert st["beta"] == rs["beta"]
+    x, rx = g.get_x().cpu().numpy(), r.x()
+    assert np.max(np.abs(x - rx)) <= 1e-4 * max(1.0, np.max(np.abs(rx)))
+    rub, _ = r.anchors()
+    assert np.max(np.abs(ub.cpu().numpy() - rub)) <= 1e-3 * max(1.0, np.max(np.abs(rub)))
+    assert st["lp_obj"][-1] == pytest.approx(rs["lp_obj"][-1], rel=1e-4)

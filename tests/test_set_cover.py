@@ -165,6 +165,16 @@ def test_set_cover_rounding_cross_application():
             assert res["feasible"] == rres["feasible"] == 1
             for k in ("cost", "eps_or_alpha", "fallback", "rounds", "n_selected"):
                 assert res[k] == rres[k], k
+    # an element in no set cannot be covered: both sides report an infeasible rounding
+    members2 = members[:100] + [[]] + members[100:200]
+    cp2, ri2, rp2, ci2 = covering_lp_arrays(n_sets, members2)
+    o2 = np.ones(len(ri2), np.float32)
+    g2 = th.LP.from_csc_csr(len(members2), n_sets, cp2, ri2, o2, rp2, ci2, o2, np.ones(len(members2), np.float32),
+                            cost, sense=np.full(len(members2), th.THETIS_GE, np.int8))
+    r2 = ref_cover_lp(n_sets, members2, cost, bits=32)
+    sel, res = g2.round_x(xs[1], th.THETIS_ROUND_SC_THRESHOLD)
+    rsel, rres = r2.round_x(xs[1], th.THETIS_ROUND_SC_THRESHOLD)
+    assert np.array_equal(sel.cpu().numpy(), rsel) and res["feasible"] == rres["feasible"] == 0
     bad = th.LP.from_csc_csr(n_elem, n_sets, colptr, rowidx, ones, rowptr, colidx, ones,
                              np.full(n_elem, 2.0, np.float32), cost, sense=np.full(n_elem, th.THETIS_GE, np.int8))
     with pytest.raises(th.ThetisError):
