@@ -72,11 +72,20 @@ __global__ void k_colour_init(DevLP L, int64_t S, int32_t* colour) {
         colour[u] = (L.unit_fixed && L.unit_fixed[u]) ? -2 : -1;
 }
 
+// units whose columns hold more than kLongUnit nonzeros are scanned by a warp each
+// (k_jp_round_long); the others by one thread
+constexpr int64_t kLongUnit = 256;
+__device__ __forceinline__ int64_t unit_nnz(const DevLP& L, int64_t u) {
+    int64_t first, cnt;
+    if (u < L.n_blocks) { first = u * L.k; cnt = L.k; }
+    else { first = L.n_blocks * L.k + (u - L.n_blocks); cnt = 1; }
+    return L.colptr[first + cnt] - L.colptr[first];
+}
 __global__ void k_jp_round(DevLP L, int64_t S, const uint64_t* __restrict__ rank, int32_t* colour,
                            unsigned long long* remaining) {
     unsigned long long left = 0;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x) {
-        if (colour[u] != -1) continue;
+        if (colour[u] != -1 || unit_nnz(L, u) > kLongUnit) continue;
         const uint64_t pu = rank[u];
         int32_t base = 0;
         bool ready = true, done = false;
@@ -102,6 +111,70 @@ __global__ void k_jp_round(DevLP L, int64_t S, const uint64_t* __restrict__ rank
     }
     for (int o = 16; o; o >>= 1) left += __shfl_xor_sync(0xffffffffu, left, o);
     if ((threadIdx.x & 31) == 0 && left) atomicAdd(remaining, left);
+}
+
+// the same round for the long units (a list), one warp per unit: the lanes scan the
+// unit's entries strided, the warp combines "every higher-priority neighbour is
+// coloured" and the used colours of each 64-colour window
+__global__ void k_jp_round_long(DevLP L, const int32_t* __restrict__ units, int64_t n_units,
+                                const uint64_t* __restrict__ rank, int32_t* colour, unsigned long long* remaining) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = w0; q < n_units; q += nw) {
+        const int64_t u = units[q];
+        if (colour[u] != -1) continue;
+        const uint64_t pu = rank[u];
+        int64_t first, cnt;
+        if (u < L.n_blocks) { first = u * L.k; cnt = L.k; }
+        else { first = L.n_blocks * L.k + (u - L.n_blocks); cnt = 1; }
+        int32_t base = 0;
+        bool done = false, ready = true;
+        while (!done && ready) {
+            unsigned long long mask = 0;
+            bool lane_ready = true;
+            for (int64_t j = first; j < first + cnt && lane_ready; j++)
+                for (int64_t t = L.colptr[j] + lane; t < L.colptr[j + 1] && lane_ready; t += 32) {
+                    const int64_t i = (int64_t)((uint32_t)L.rowidx[t] & kRowMask);
+                    auto visit = [&](int64_t w) {
+                        if (w == u || !precedes(rank[w], w, pu, u)) return;
+                        const int32_t cw = ((volatile int32_t*)colour)[w];
+                        if (cw == -2) return;
+                        if (cw == -1) { lane_ready = false; return; }
+                        if (cw >= base && cw < base + 64) mask |= 1ull << (cw - base);
+                    };
+                    if (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) {
+                        const int2 e = L.edges[i];
+                        visit(e.x == (int32_t)u ? e.y : e.x);
+                    } else if (L.problem == THETIS_PROB_MWC) {
+                        const int64_t k = L.k, e = i / (2 * k), l = (i >> 1) % k;
+                        const int2 uv = L.edges[e];
+                        visit((int64_t)uv.x);
+                        visit((int64_t)uv.y);
+                        visit(L.n_blocks + e * k + l);
+                    } else {
+                        for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; p++) visit(unit_of_col(L, L.rcol[p]));
+                    }
+                }
+            ready = __all_sync(0xffffffffu, lane_ready);
+            if (!ready) break;
+            const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)mask);
+            const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(mask >> 32));
+            const unsigned long long m = ((unsigned long long)hi << 32) | lo;
+            if (m != ~0ull) {
+                if (lane == 0) colour[u] = base + __ffsll((long long)~m) - 1;
+                done = true;
+            } else {
+                base += 64;
+            }
+        }
+        if (!done && lane == 0) atomicAdd(remaining, 1ull);
+    }
+}
+// the long units (unordered list)
+__global__ void k_long_units(DevLP L, int64_t S, int32_t* units, unsigned long long* count) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < S; u += (int64_t)gridDim.x * blockDim.x)
+        if (unit_nnz(L, u) > kLongUnit) units[atomicAdd(count, 1ull)] = (int32_t)u;
 }
 
 __global__ void k_colour_max(int64_t S, const int32_t* colour, int32_t* out) {
@@ -146,9 +219,22 @@ int ensure_colouring(thetis_lp* lp, uint64_t seed) {
         if ((size_t)S * 8 > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "colouring ranks");
         k_colour_rank<<<grid_for(S, T), T, 0, s>>>(L, S, key, rank);
         k_colour_init<<<grid_for(S, T), T, 0, s>>>(L, S, lp->colour);
+        int32_t* long_units = (int32_t*)(rank + S);
+        unsigned long long n_long = 0;
+        if ((size_t)S * 12 > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "colouring ranks");
+        {
+            unsigned long long* cnt = (unsigned long long*)(lp->flags + 34);
+            CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
+            k_long_units<<<grid_for(S, T), T, 0, s>>>(L, S, long_units, cnt);
+            CUDA_TRY(lp, cudaMemcpyAsync(&n_long, cnt, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+        }
         for (int round = 0;; round++) {
             CUDA_TRY(lp, cudaMemsetAsync(remaining, 0, 8, s));
             k_jp_round<<<grid_for(S, T), T, 0, s>>>(L, S, rank, lp->colour, remaining);
+            if (n_long > 0)
+                k_jp_round_long<<<grid_for(32 * (int64_t)n_long, T), T, 0, s>>>(L, long_units, (int64_t)n_long, rank,
+                                                                               lp->colour, remaining);
             unsigned long long left = 0;
             CUDA_TRY(lp, cudaMemcpyAsync(&left, remaining, 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));
