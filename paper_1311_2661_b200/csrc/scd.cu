@@ -1074,12 +1074,15 @@ __device__ void process_tile(const DevLP& L, const StepParams& P, const AsyncCtx
 #ifndef THETIS_ASYNC_MINB
 #define THETIS_ASYNC_MINB 6
 #endif
+#ifndef THETIS_BLOCKS_MINB
+#define THETIS_BLOCKS_MINB 3
+#endif
 // kPath: kPathBlocks (the LP has simplex blocks: MWC), kPathScalar (scalar columns,
 // no lv: lane-per-column or warp-cooperative tiles), kPathLight (light tiles with lv)
 enum { kPathBlocks = 0, kPathScalar = 1, kPathLight = 2, kPathBlocks8 = 3 /* host side: blocks, k <= 8 */ };
 // KC: block capacity (kPathBlocks: 8 for k <= 8, registers; kMaxK otherwise)
 template <int kPath, int KC = 1>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? (KC <= 8 ? 3 : 1) : THETIS_ASYNC_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPath == kPathBlocks ? (KC <= 8 ? THETIS_BLOCKS_MINB : 1) : THETIS_ASYNC_MINB)
     k_async(DevLP L, StepParams P, AsyncCtx C, int batch, int64_t n_workers) {
     constexpr bool kBlocks = kPath == kPathBlocks;
     __shared__ WarpSmem wsm[kWarpsPerBlock];
