@@ -89,9 +89,10 @@ typedef struct {
     double L_max;               /* Eq. 7 */
     int64_t n_colours;          /* deterministic mode: classes before the slack class */
     int32_t mode, step_rule;
-    /* async mode with a hub step, over the first 64 epochs (CUDA events on the solve
-     * stream): device time of the row passes (plus the call's final application of
-     * the pending steps), of the hub updates, and of the permuted tiles */
+    /* async mode, over the first 64 epochs (CUDA events on the solve stream): device
+     * time of the row passes (plus the call's final application of the pending steps;
+     * without a hub step: the slack sweeps), of the hub updates, and of the permuted
+     * tiles */
     double ms_row_pass, ms_hub_update, ms_tiles;
     int64_t row_pass_launches;
 } thetis_solve_stats;

@@ -1464,8 +1464,10 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 THETIS_TRY(kern_mark(e, 0));
                 k_hub_update<<<hb, 256, 0, s>>>(L, P, H);
                 THETIS_TRY(kern_mark(e, 1));
-            } else if (L.n_ineq > 0) {
-                k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
+            } else {
+                if (L.n_ineq > 0) k_slack_sweep<<<grid_for(L.n_ineq, 256, 148 * 8), 256, 0, s>>>(L, P);
+                THETIS_TRY(kern_mark(e, 0));  // (no hub step: the slack sweep stands for the row pass)
+                THETIS_TRY(kern_mark(e, 1));
             }
             // (3) the permuted tiles of structural units
             if (n_tiles > 0) {
@@ -1477,7 +1479,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 else k_async<kPathLight><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, s>>>(L, P, AC, batch, workers);
             }
         }
-        if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) THETIS_TRY(kern_mark(e, 2));
+        if (mode != THETIS_MODE_DETERMINISTIC) THETIS_TRY(kern_mark(e, 2));
         // the last epoch's hub steps are still pending: apply them, r = A z - b again
         if (e == epochs - 1 && mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
             CUDA_TRY(lp, cudaMemsetAsync(H.next, 0, 8, s));
@@ -1500,7 +1502,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             CUDA_TRY(lp, cudaEventElapsedTime(&ms, lp->ev_epoch[e], lp->ev_epoch[e + 1]));
             st->ms_per_epoch[e] = ms;
             st->ms_total += ms;
-            if (mode != THETIS_MODE_DETERMINISTIC && H.n_heavy > 0) {
+            if (mode != THETIS_MODE_DETERMINISTIC) {
                 float a = 0, b = 0, c = 0;
                 CUDA_TRY(lp, cudaEventElapsedTime(&a, lp->ev_epoch[e], lp->ev_kern[3 * e]));
                 CUDA_TRY(lp, cudaEventElapsedTime(&b, lp->ev_kern[3 * e], lp->ev_kern[3 * e + 1]));
@@ -1509,7 +1511,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                 st->ms_hub_update += b;
                 st->ms_tiles += c;
                 st->row_pass_launches += 1;
-                if (e == epochs - 1) {  // the final application of the pending steps
+                if (e == epochs - 1 && H.n_heavy > 0) {  // the final application of the pending steps
                     float f = 0;
                     CUDA_TRY(lp, cudaEventElapsedTime(&f, lp->ev_kern[3 * e + 2], lp->ev_epoch[e + 1]));
                     st->ms_row_pass += f;
