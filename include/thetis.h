@@ -76,7 +76,9 @@ enum { THETIS_ROUND_VC_HALF = 1,   /* Lemma-1 threshold (1-eps)/2 + fix-up (P:13
        THETIS_ROUND_MIS_GREEDY = 3,/* packing alpha + greedy repair */
        THETIS_ROUND_MWC_CKR = 4,   /* CKR region growing, best of reps */
        THETIS_ROUND_SC_THRESHOLD = 5, /* set cover: x_s >= (1-eps)/f + fix-up (App. B.1; R-20) */
-       THETIS_ROUND_SC_RANDOM = 6     /* set cover: keep s w.p. min(1, d x_s) + fix-up (App. B.1; R-20) */ };
+       THETIS_ROUND_SC_RANDOM = 6,    /* set cover: keep s w.p. min(1, d x_s) + fix-up (App. B.1; R-20) */
+       THETIS_ROUND_MIS_BANSAL = 7    /* MIS: Bansal et al.'s Alg. 2 with theta = 1/k on x/(1+alpha), best of reps
+                                         (R-21) */ };
 
 #define THETIS_MAX_EPOCH_TIMES 64
 
@@ -248,7 +250,13 @@ THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float b
  * (SplitMix64 of seed ^ 0x5851F42D4C957F2D (s + 1)), fallback = 1 when that sample
  * left an element uncovered.  Both then add, for every uncovered element, its set
  * with the largest x (ties: smaller cost, then smaller index), judged against the
- * pre-fix-up selection; rounds = sets added, eps_or_alpha = eps. */
+ * pre-fix-up selection; rounds = sets added, eps_or_alpha = eps.
+ * MIS_BANSAL (NEXT-2, R-21): alpha and x~ = x/(1+alpha) as MIS_GREEDY; repetition t keeps
+ * vertex v iff u_{t,v} < x~_v (Alg. 2 step 2 with k theta = 1), u_{t,v} the v-th SplitMix64
+ * output seeded seed ^ 0xC2B2AE3D27D4EB4F (t+1), as ((h >> 40) + 1/2) 2^-24; a kept vertex
+ * with a kept neighbour is deleted (steps 3-4 for unit weights: E_{a,v} when another chosen
+ * set holds a); the best of `reps` (1..64) by weight (ties: smaller t) is returned;
+ * best_rep = t, eps_or_alpha = alpha. */
 THETIS_API int thetis_round(thetis_lp* lp, int rule, uint64_t seed, int reps, uint8_t* out_assign,
                             thetis_round_result* out /* host */);
 /* Same on an explicit structural point x float[n_struct] (host or device). */

@@ -19,7 +19,7 @@ PROB_VC, PROB_MIS, PROB_MWC = 1, 2, 3
 MODE_DET, MODE_ASYNC, MODE_CYCLIC, MODE_TILE_SYNC = 0, 1, 2, 3
 STEP_LMAX, STEP_LJ = 0, 1
 ROUND_VC_HALF, ROUND_VC_FIXUP, ROUND_MIS_GREEDY, ROUND_MWC_CKR = 1, 2, 3, 4
-ROUND_SC_THRESHOLD, ROUND_SC_RANDOM = 5, 6
+ROUND_SC_THRESHOLD, ROUND_SC_RANDOM, ROUND_MIS_BANSAL = 5, 6, 7
 SENSE_EQ, SENSE_GE, SENSE_LE = 0, 1, 2
 
 

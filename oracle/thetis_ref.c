@@ -27,7 +27,7 @@ enum { OBJ_MIN = 0, OBJ_MAX = 1 };
 enum { MODE_DET = 0, MODE_ASYNC = 1, MODE_CYCLIC = 2 };
 enum { STEP_LMAX = 0, STEP_LJ = 1 };
 enum { ROUND_VC_HALF = 1, ROUND_VC_FIXUP = 2, ROUND_MIS_GREEDY = 3, ROUND_MWC_CKR = 4, ROUND_SC_THRESHOLD = 5,
-       ROUND_SC_RANDOM = 6 };
+       ROUND_SC_RANDOM = 6, ROUND_MIS_BANSAL = 7 };
 
 struct ref_lp {
     int problem;
@@ -1089,9 +1089,60 @@ static int round_set_cover(const ref_lp* lp, const float* x, int rule, uint64_t 
     return REF_OK;
 }
 
+/* MIS by Bansal et al.'s Alg. 2 as the paper ran it (
+ * DESIGN.md R-21): x~ = x/(1+alpha) (the packing lemma's feasible point, tight alpha of
+ * P:1313-1315); theta = 1/k, so step 2 keeps vertex v with probability x~_v / (k theta)
+ * = x~_v, drawn as u_{t,v} < x~_v with u_{t,v} = ((h >> 40) + 1/2) 2^-24, h the v-th
+ * SplitMix64 output seeded seed ^ 0xC2B2AE3D27D4EB4F (t+1); steps 3-4 with unit weights
+ * (w_{a,s} = 1 for an edge a at vertex s): a kept vertex with a kept neighbour is deleted
+ * (the event that the other chosen sets holding a exceed the capacity left by s; the
+ * literal strict "> w_{a,s}" never fires for unit weights, A-10); the best of `reps`
+ * repetitions by weight, ties to the smaller t. */
+static int round_mis_bansal(const ref_lp* lp, const float* x, uint64_t seed, int reps, uint8_t* out,
+                            ref_round_result* res) {
+    if (lp->problem != PROB_MIS) return REF_NOT_SUPPORTED;
+    if (reps < 1 || reps > 64) return REF_INVALID_ARG;
+    const int64_t n = lp->n_vert, me = lp->m_edges;
+    float alpha = 0.0f;
+    for (int64_t e = 0; e < me; e++) {
+        float v = (x[lp->eu[e]] + x[lp->ev[e]]) - 1.0f;
+        if (v > alpha) alpha = v;
+    }
+    const float scale = 1.0f + alpha;
+    uint8_t* keep = (uint8_t*)xcalloc(n + 1, 1);
+    uint8_t* best_sel = (uint8_t*)xcalloc(n + 1, 1);
+    double best_w = -1.0;
+    int best_t = 0;
+    for (int t = 0; t < reps; t++) {
+        const uint64_t st = seed ^ (0xC2B2AE3D27D4EB4FULL * (uint64_t)(t + 1));
+        for (int64_t v = 0; v < n; v++) {
+            float p = x[v] / scale;
+            float u = ((float)(sm64_out(st, (uint64_t)v) >> 40) + 0.5f) * (1.0f / 16777216.0f);
+            keep[v] = u < p ? 1 : 0;
+        }
+        uint8_t* sel = (uint8_t*)xcalloc(n + 1, 1);
+        for (int64_t v = 0; v < n; v++) sel[v] = keep[v];
+        for (int64_t e = 0; e < me; e++)
+            if (keep[lp->eu[e]] && keep[lp->ev[e]]) { sel[lp->eu[e]] = 0; sel[lp->ev[e]] = 0; }
+        double w = 0.0;
+        for (int64_t v = 0; v < n; v++) if (sel[v]) w += (double)lp->vw[v];
+        if (w > best_w) { best_w = w; best_t = t; memcpy(best_sel, sel, (size_t)n); }
+        free(sel);
+    }
+    int64_t cnt = 0;
+    for (int64_t v = 0; v < n; v++) { out[v] = best_sel[v]; cnt += best_sel[v]; }
+    int64_t feas = 1;
+    for (int64_t e = 0; e < me; e++) if (out[lp->eu[e]] && out[lp->ev[e]]) feas = 0;
+    res->cost = best_w; res->n_selected = cnt; res->best_rep = best_t; res->eps_or_alpha = (double)alpha;
+    res->feasible = feas;
+    free(keep); free(best_sel);
+    return REF_OK;
+}
+
 int thetis_ref_round_x(const ref_lp* lp, const float* x, int rule, uint64_t seed, int reps,
                        uint8_t* out, ref_round_result* res) {
     memset(res, 0, sizeof(*res));
+    if (rule == ROUND_MIS_BANSAL) return round_mis_bansal(lp, x, seed, reps, out, res);
     if (rule == ROUND_SC_THRESHOLD || rule == ROUND_SC_RANDOM) return round_set_cover(lp, x, rule, seed, out, res);
     int64_t n = lp->n_vert, me = lp->m_edges;
     if (rule == ROUND_VC_HALF || rule == ROUND_VC_FIXUP) {

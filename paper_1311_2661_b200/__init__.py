@@ -36,7 +36,7 @@ THETIS_PROB_GENERIC, THETIS_PROB_VC, THETIS_PROB_MIS, THETIS_PROB_MWC = 0, 1, 2,
 THETIS_MODE_DETERMINISTIC, THETIS_MODE_ASYNC, THETIS_MODE_ASYNC_SERIAL = 0, 1, 2
 THETIS_STEP_LMAX, THETIS_STEP_LJ = 0, 1
 THETIS_ROUND_VC_HALF, THETIS_ROUND_VC_FIXUP, THETIS_ROUND_MIS_GREEDY, THETIS_ROUND_MWC_CKR = 1, 2, 3, 4
-THETIS_ROUND_SC_THRESHOLD, THETIS_ROUND_SC_RANDOM = 5, 6
+THETIS_ROUND_SC_THRESHOLD, THETIS_ROUND_SC_RANDOM, THETIS_ROUND_MIS_BANSAL = 5, 6, 7
 THETIS_MAX_EPOCH_TIMES = 64
 
 LIB_PATH = _LIB_PATH

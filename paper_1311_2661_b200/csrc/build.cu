@@ -526,7 +526,7 @@ size_t post_build_temp(int64_t S, int64_t n_struct, int64_t n_vert) {
     size_t colour = 8 * 256 + 5 * ((size_t)S + 2) * 4 + mx + 4 * 256;
     // (selection bytes: per vertex, or per set for the set-cover rules)
     size_t round = 8 * 256 + (size_t)n_struct * 4 + 2 * (size_t)(n_vert > n_struct ? n_vert : n_struct) +
-                   (size_t)64 * kRedBlocks * 8 + 64 * 8 + 64 + 32;
+                   (size_t)64 * kRedBlocks * 8 + 64 * 8 + 64 + 32 + 16 * (size_t)n_vert + 512;  // + MIS_BANSAL masks
     return colour > round ? colour : round;
 }
 

@@ -195,6 +195,57 @@ __global__ void k_sc_bad_rows(const DevLP L, const uint8_t* __restrict__ sel, un
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
 }
 
+// ---------------- MIS, Bansal et al.'s Alg. 2 (theta = 1/k): bit t of mask[v] = v
+// chosen in repetition t; a chosen vertex with a chosen neighbour is deleted
+__device__ __forceinline__ float bansal_uniform(uint64_t seed, int t, int64_t v) {
+    const uint64_t st = seed ^ (0xC2B2AE3D27D4EB4FULL * (uint64_t)(t + 1));
+    return ((float)(sm64_mix(st + (uint64_t)(v + 1) * kGolden) >> 40) + 0.5f) * (1.0f / 16777216.0f);
+}
+__global__ void k_bansal_sample(int64_t n, const float* __restrict__ x, const float* alpha_p, uint64_t seed, int reps,
+                                unsigned long long* mask, unsigned long long* del) {
+    const float scale = __fadd_rn(1.0f, *alpha_p);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const float p = __fdiv_rn(x[v], scale);  // x~ = x / (1 + alpha), probability x~ / (k theta)
+        unsigned long long b = 0;
+        for (int t = 0; t < reps; t++)
+            if (bansal_uniform(seed, t, v) < p) b |= 1ull << t;
+        mask[v] = b;
+        del[v] = 0;
+    }
+}
+__global__ void k_bansal_conflicts(int64_t m, const int2* __restrict__ edges, const unsigned long long* __restrict__ mask,
+                                   unsigned long long* del) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const int2 uv = edges[e];
+        const unsigned long long c = mask[uv.x] & mask[uv.y];
+        if (c) {
+            atomicOr(del + uv.x, c);
+            atomicOr(del + uv.y, c);
+        }
+    }
+}
+__global__ void __launch_bounds__(T) k_bansal_weight(int64_t n, const float* __restrict__ w,
+                                                     const unsigned long long* __restrict__ mask,
+                                                     const unsigned long long* __restrict__ del, double* partial) {
+    const int t = blockIdx.y;
+    double acc = 0.0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (((mask[v] & ~del[v]) >> t) & 1ull) acc += (double)w[v];
+    __shared__ double sh[T];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int off = T / 2; off > 0; off >>= 1) {
+        if ((int)threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[(int64_t)t * gridDim.x + blockIdx.x] = sh[0];
+}
+__global__ void k_bansal_select(int64_t n, const unsigned long long* __restrict__ mask,
+                                const unsigned long long* __restrict__ del, int best, uint8_t* sel) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        sel[v] = (uint8_t)(((mask[v] & ~del[v]) >> best) & 1ull);
+}
+
 // ---------------- MIS
 __global__ void k_mis_alpha(int64_t m, const int2* __restrict__ edges, const float* __restrict__ x, float* alpha) {
     float best = 0.0f;
@@ -394,6 +445,46 @@ int round_x(thetis_lp* lp, const float* x, int rule, uint64_t seed, int reps, ui
         res->n_selected = (int64_t)h[1];
         res->eps_or_alpha = ha;
         res->rounds = rounds;
+        res->feasible = bad == 0;
+    } else if (rule == THETIS_ROUND_MIS_BANSAL) {
+        if (L.problem != THETIS_PROB_MIS) return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "MIS rounding needs an MIS LP");
+        if (reps < 1 || reps > kMaxReps) return set_error(lp, THETIS_ERR_INVALID_ARG, "reps must be in [1, 64]");
+        float* alpha = (float*)small;
+        Carver C2(lp->temp);
+        C2.take<char>((int64_t)C.off);  // after this call's rounding temporaries
+        unsigned long long* mask = C2.take<unsigned long long>(n > 0 ? n : 1);
+        unsigned long long* del = C2.take<unsigned long long>(n > 0 ? n : 1);
+        if (C2.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "rounding temp");
+        if (m > 0) k_mis_alpha<<<ge, T, 0, s>>>(m, L.edges, x, alpha);
+        if (n > 0) k_bansal_sample<<<gv, T, 0, s>>>(n, x, alpha, seed, reps, mask, del);
+        if (m > 0) k_bansal_conflicts<<<ge, T, 0, s>>>(m, L.edges, mask, del);
+        const int blocks = kRedBlocks;
+        dim3 grid(blocks, reps);
+        k_bansal_weight<<<grid, T, 0, s>>>(n, L.c, mask, del, partial);
+        k_mwc_cost_final<<<1, kMaxReps, 0, s>>>(reps, blocks, partial, sums);
+        double hw[kMaxReps];
+        float ha;
+        CUDA_TRY(lp, cudaMemcpyAsync(hw, sums, (size_t)reps * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaMemcpyAsync(&ha, alpha, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        int best = 0;
+        for (int t = 1; t < reps; t++)
+            if (hw[t] > hw[best]) best = t;
+        if (n > 0) k_bansal_select<<<gv, T, 0, s>>>(n, mask, del, best, selp);
+        CUDA_TRY(lp, cudaMemsetAsync(add, 0, (size_t)(n > 0 ? n : 1), s));
+        k_vc_merge<<<kRedBlocks, T, 0, s>>>(n, L.c, selp, add, partial);
+        k_sum_partials<<<1, 32, 0, s>>>(kRedBlocks, 2, partial, sums);
+        CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
+        if (m > 0) k_count_bad_edges<<<ge, T, 0, s>>>(m, L.edges, selp, 0, cnt);
+        double h[2];
+        unsigned long long bad;
+        CUDA_TRY(lp, cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaMemcpyAsync(&bad, cnt, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        res->cost = hw[best];
+        res->n_selected = (int64_t)h[1];
+        res->eps_or_alpha = ha;
+        res->best_rep = best;
         res->feasible = bad == 0;
     } else if (rule == THETIS_ROUND_MWC_CKR) {
         if (L.problem != THETIS_PROB_MWC) return set_error(lp, THETIS_ERR_NOT_SUPPORTED, "MWC rounding needs an MWC LP");
