@@ -101,13 +101,27 @@ def main():
         alg = 20 * lp.n_struct + 12 * lp.nnz_struct + 16 * lp.n_ineq
         ob = lp.objective(cfg.beta)
         extra = {}
+        rules = {1: [("VC_HALF", th.THETIS_ROUND_VC_HALF)], 2: [("MIS_GREEDY", th.THETIS_ROUND_MIS_GREEDY),
+                                                                 ("MIS_BANSAL", th.THETIS_ROUND_MIS_BANSAL)],
+                 3: [("MWC_CKR", th.THETIS_ROUND_MWC_CKR)]}.get(prob, [])
+        for rname, rule in rules:  # device time of one rounding call (CUDA events, 10 repetitions)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            lp.round(rule, seed=3, reps=10)  # warm-up
+            e0.record(lp.stream)
+            _, rr = lp.round(rule, seed=3, reps=10)
+            e1.record(lp.stream)
+            e1.synchronize()
+            extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
         if name == "sc_1m":
-            import time
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            _, rr = lp.round(th.THETIS_ROUND_SC_THRESHOLD)
-            extra = dict(round_ms=(time.perf_counter() - t0) * 1e3, cover_cost=rr["cost"], feasible=rr["feasible"],
-                         lp_obj=ob["lp_obj"], eps=ob["max_violation_eps"])
+            for rname, rule in (("SC_THRESHOLD", th.THETIS_ROUND_SC_THRESHOLD), ("SC_RANDOM", th.THETIS_ROUND_SC_RANDOM)):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                lp.round(rule, seed=3)
+                e0.record(lp.stream)
+                _, rr = lp.round(rule, seed=3)
+                e1.record(lp.stream)
+                e1.synchronize()
+                extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
+            extra.update(lp_obj=ob["lp_obj"], eps=ob["max_violation_eps"])
         out = dict(config=name, mode="det" if mode == 0 else "async", epochs=epochs, ms_epoch_median=med,
                    ms_epoch_first=ms[0], updates_per_s=upd / med * 1e3, nnz_per_s=nnz / med * 1e3,
                    alg_bytes_per_epoch=alg, alg_GBps=alg / med / 1e6, frac_of_measured_hbm=alg / med / 1e6 / peak,
