@@ -79,6 +79,8 @@ def main():
         k2 = torch.unique((v[sel] >> 14) * (1 << 32) + u[sel])
         out["min_pairs_v_ranged"] = int(k2.numel())
         # distinct (range_u, v) pairs of all rows with hub v
+        for lg in (18, 20, 22):  # rows with both endpoints below 2^lg (a dense corner for 2D tiling)
+            out["rows_both_below_2^%d" % lg] = int(((u < (1 << lg)) & (v < (1 << lg))).sum())
         del u, v, key, k2, eu, ev
         torch.cuda.empty_cache()
     st = th.SolveStats()
