@@ -595,3 +595,23 @@ def test_fp32_build_tracks_fp64_build():
         lp.solve(10.0, 20, mode=oracle.MODE_DET, seed=71)
     assert np.abs(a.x() - b.x()).max() < 1e-6
     assert np.abs(a.r() - b.r()).max() < 1e-6
+
+
+def test_column_dot_is_the_contracts_tree():
+    # R-7: lanes at CSC positions 0, 1, 2 combine by halving, off = 2 first:
+    # p0 = (r0 + r2) + r1.  With r = (1e8, 1, -1e8) in fp32 that is (1e8 - 1e8) + 1 = 1,
+    # while the plain sequential sum (1e8 + 1) - 1e8 rounds to 0 (fp32 spacing at 1e8 is 8).
+    # One EQ row per entry, b = -r, z = 0, c = 0, beta = 1: the gradient is the dot itself.
+    b = np.array([-1e8, -1.0, 1e8], np.float32)
+    lp = RefLP.generic(3, 1, np.array([0, 3]), np.array([0, 1, 2], np.int32), np.ones(3, np.float32), b,
+                       np.zeros(1, np.float32), sense=np.zeros(3, np.int8), bits=32)
+    assert lp.r().tolist() == [1e8, 1.0, -1e8]
+    assert lp.grad(1.0, 0) == 1.0
+    # 1025 entries: lane 0 also takes position 1024, added after position 0 (in CSC order)
+    n = 1025
+    rr = np.zeros(n, np.float32)
+    rr[0], rr[1024], rr[512] = 1e8, 1.0, -1e8
+    lp = RefLP.generic(n, 1, np.array([0, n]), np.arange(n, dtype=np.int32), np.ones(n, np.float32), -rr,
+                       np.zeros(1, np.float32), sense=np.zeros(n, np.int8), bits=32)
+    # lane 0 = fl(1e8 + 1) = 1e8; lane 512 = -1e8; off = 512: 1e8 + (-1e8) = 0 -> D = 0
+    assert lp.grad(1.0, 0) == 0.0

@@ -451,3 +451,22 @@ def test_errors(th):
     with pytest.raises(th.ThetisError) as e:
         g.round(3)
     assert e.value.code == th.THETIS_ERR_NOT_SUPPORTED
+
+
+@pytest.mark.parametrize("n", [3, 1025, 9000])
+def test_det_column_dot_order_cases(th, n):
+    # the contract's lane order decides these sums (see test_column_dot_is_the_contracts_tree):
+    # one column over n EQ rows with large cancelling residuals; thread (3), warp (1025) and
+    # CTA (9000 > 8192) paths must give the oracle's bits
+    rr = np.zeros(n, np.float32)
+    rr[0], rr[n // 2], rr[n - 1] = 1e8, -1e8, 1.0
+    rr[1:n - 1:7] += 0.25
+    colptr, rowidx = np.array([0, n]), np.arange(n, dtype=np.int32)
+    args = (n, 1, colptr, rowidx, np.ones(n, np.float32))
+    g = th.LP.from_csc_csr(*args, np.arange(n + 1, dtype=np.int64), np.zeros(n, np.int32), np.ones(n, np.float32),
+                           -rr, np.ones(1, np.float32), sense=np.zeros(n, np.int8))
+    r32 = RefLP.generic(*args, -rr, np.ones(1, np.float32), sense=np.zeros(n, np.int8), bits=32)
+    g.solve(1.0, 2, mode=th.THETIS_MODE_DETERMINISTIC, seed=1)
+    r32.solve(1.0, 2, mode=oracle.MODE_DET, seed=1)
+    assert np.array_equal(g.get_x().cpu().numpy(), r32.x32())
+    assert np.array_equal(g.get_r().cpu().numpy(), r32.r32())
