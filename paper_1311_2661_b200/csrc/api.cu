@@ -61,6 +61,10 @@ int new_handle(thetis_lp** out, void* ws, size_t ws_bytes, void* stream, thetis_
 
 void destroy(thetis_lp* lp) {
     if (!lp) return;
+    if (lp->det_graph) {
+        cudaStreamSynchronize(lp->stream);
+        cudaGraphExecDestroy(lp->det_graph);
+    }
     if (lp->side) cudaStreamDestroy(lp->side);
     if (lp->ev_fork) cudaEventDestroy(lp->ev_fork);
     if (lp->ev_join) cudaEventDestroy(lp->ev_join);

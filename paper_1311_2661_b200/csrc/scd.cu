@@ -1441,19 +1441,45 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         if (timed && e < n_timed) CUDA_TRY(lp, cudaEventRecord(lp->ev_kern[3 * e + k], s));
         return THETIS_OK;
     };
+    // det: one epoch = the class launches (identical every epoch), captured once into a
+    // CUDA graph (on the side stream) and replayed per epoch: a launch-bound epoch on small
+    // LPs pays one graph launch instead of K + 1 kernel launches
+    auto det_epoch = [&](cudaStream_t q) {
+        for (int64_t c = 0; c < lp->K; c++) {
+            int64_t beg = lp->class_ptr[c], cnt = lp->class_ptr[c + 1] - beg;
+            if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
+            else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
+            const int64_t nm = mid_ptr[c + 1] - mid_ptr[c], nl = long_ptr[c + 1] - long_ptr[c];
+            if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, q>>>(L, P, mid_cols + mid_ptr[c], nm);
+            if (nl > 0) k_det_long<<<(unsigned)nl, 1024, 0, q>>>(L, P, long_cols + long_ptr[c]);
+        }
+        if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, q>>>(L, P);
+    };
+    // (the previous call's graph is released here, after its launches completed; the last
+    // one by thetis_free)
+    if (lp->det_graph) {
+        CUDA_TRY(lp, cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(lp->det_graph);
+        lp->det_graph = nullptr;
+    }
+    cudaGraphExec_t det_graph = nullptr;
+    if (mode == THETIS_MODE_DETERMINISTIC && epochs > 1 && lp->side) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(lp->side, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            det_epoch(lp->side);
+            if (cudaStreamEndCapture(lp->side, &g) == cudaSuccess && g) {
+                if (cudaGraphInstantiate(&det_graph, g, 0) != cudaSuccess) det_graph = nullptr;
+                cudaGraphDestroy(g);
+            }
+        }
+        cudaGetLastError();  // a failed capture falls back to direct launches
+    }
     cudaEvent_t ev_start = timed ? lp->ev_epoch[0] : nullptr;
     if (timed) CUDA_TRY(lp, cudaEventRecord(ev_start, s));
     for (int e = 0; e < epochs; e++) {
         if (mode == THETIS_MODE_DETERMINISTIC) {
-            for (int64_t c = 0; c < lp->K; c++) {
-                int64_t beg = lp->class_ptr[c], cnt = lp->class_ptr[c + 1] - beg;
-                if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
-                else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, s>>>(L, P, lp->members + beg, cnt);
-                const int64_t nm = mid_ptr[c + 1] - mid_ptr[c], nl = long_ptr[c + 1] - long_ptr[c];
-                if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, s>>>(L, P, mid_cols + mid_ptr[c], nm);
-                if (nl > 0) k_det_long<<<(unsigned)nl, 1024, 0, s>>>(L, P, long_cols + long_ptr[c]);
-            }
-            if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, s>>>(L, P);
+            if (det_graph) CUDA_TRY(lp, cudaGraphLaunch(det_graph, s));
+            else det_epoch(s);
         } else {
             // (1) hub step + (2) slack sweep, fused; or (2) alone
             if (H.n_heavy > 0) {
@@ -1487,6 +1513,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));
     }
+    lp->det_graph = det_graph;
     THETIS_TRY(check_cuda(lp, "solve"));
     if (timed) {
         CUDA_TRY(lp, cudaStreamSynchronize(s));

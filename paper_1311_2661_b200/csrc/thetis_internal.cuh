@@ -261,6 +261,7 @@ struct thetis_lp {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // second stream: hub-hub row pass beside the light tiles
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaGraphExec_t det_graph = nullptr;  // the last deterministic solve's epoch graph
     std::vector<cudaEvent_t> ev_epoch;
     std::vector<cudaEvent_t> ev_kern;   // per-kernel marks of timed async epochs
     char* ws = nullptr;
