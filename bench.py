@@ -165,10 +165,10 @@ def run_thetis(args):
     import paper_1311_2661_b200 as th
 
     ws_n, rank, local = dist_env()
+    torch.cuda.set_device(local)  # before the process group: NCCL binds each rank to its own GPU
     if ws_n > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg = inputs.CONFIGS[CFG_NAME]
     p = dict(cfg.params)
