@@ -3,8 +3,9 @@
 
 A step is one pass of the whole hot path over one synthetic instance of the
 workload: LP build from the edge list (K1-K3: canonicalise / dedup / CSC /
-L_max / r0), the SCD epochs (async Hogwild kernel, per-epoch on-device
-permutations), the fused reductions (K9) and the rounding pass (K10).
+L_max / r0), the SCD epochs (THETIS_MODE_ASYNC: Alg. 1's per-epoch permuted sweep
+run Hogwild-style, the mode whose trajectory is checked against the oracle's
+Alg. 1 in tests/), the fused reductions (K9) and the rounding pass (K10).
 The colouring (K4) belongs to the deterministic mode and is not on this
 workload's path (BASELINE: config 5 runs in async mode).
 
@@ -13,6 +14,9 @@ which the north-star target (>= 60% of the HBM roofline per epoch) is stated:
 R-MAT scale 26, 16*2^26 edge samples (a,b,c) = (0.57,0.19,0.19), weights
 U[1,10), beta = 10, 20 async epochs, Lemma-1 rounding.  Inputs are generated
 on the device (inputs/gen_cuda.cu) before timing; they exceed the 126 MB L2.
+Beside the headline, `variants` times the same 20 epochs under the hub-lag
+throughput schedule (THETIS_MODE_ASYNC_HUBLAG, R-22) and under the
+1/L_j step rule.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -50,6 +54,7 @@ def parse():
     p.add_argument("--scale", type=int, default=None, help="R-MAT scale override (testing only)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-variants", action="store_true", help="skip the hub-lag / STEP_LJ variant epochs")
     return p.parse_args()
 
 
@@ -192,13 +197,17 @@ def run_thetis(args):
     sel = torch.empty(n, dtype=torch.uint8, device=dev)
     info = {}
 
-    def step(src_p, dst_p, w_p, out_p, record=None):
+    def step(src_p, dst_p, w_p, out_p, record=None, mode=None, rule=None, start=False):
         h = ctypes.c_void_p()
         th._check(th.thetis_build_graph_lp(ctypes.byref(h), ws.data_ptr(), ws.numel(), sp, th.THETIS_PROB_VC, n, E,
                                            src_p, dst_p, w_p, None, 0, None, 0), "build")
+        if start and record is not None:  # f_beta at z0 (progress measure; outside the timed region)
+            ob0 = th.Objective()
+            th._check(th.thetis_objective(h, BETA, ctypes.byref(ob0)), "objective", h)
+            record["ob0"] = ob0
         st = th.SolveStats()
-        th._check(th.thetis_solve(h, BETA, EPOCHS, th.THETIS_MODE_ASYNC, cfg.solve_seed, th.THETIS_STEP_LMAX,
-                                  ctypes.byref(st)), "solve", h)
+        th._check(th.thetis_solve(h, BETA, EPOCHS, th.THETIS_MODE_ASYNC if mode is None else mode, cfg.solve_seed,
+                                  th.THETIS_STEP_LMAX if rule is None else rule, ctypes.byref(st)), "solve", h)
         ob = th.Objective()
         th._check(th.thetis_objective(h, BETA, ctypes.byref(ob)), "objective", h)
         rr = th.RoundResult()
@@ -215,8 +224,8 @@ def run_thetis(args):
             dist.barrier()
 
     # warm-up
-    for _ in range(args.warmup):
-        step(src.data_ptr(), dst.data_ptr(), w.data_ptr(), sel.data_ptr(), info)
+    for i in range(args.warmup):
+        step(src.data_ptr(), dst.data_ptr(), w.data_ptr(), sel.data_ptr(), info, start=i == 0)
     stream.synchronize()
     # timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -242,24 +251,30 @@ def run_thetis(args):
     value = job_throughput(upd_step, args.steps, ws_n, ms)
     ep_med = statistics.median(epoch_ms)
     # live per-kernel device time of the epoch's launches (CUDA events on the solve stream)
-    kst = [r["st"] for r in recs]
-    n_rp = sum(x.row_pass_launches for x in kst)
-    n_ep = sum(min(int(x.epochs), 64) for x in kst)
-    kernels = None
-    if n_rp:
-        kernels = {
-            "k_rows_pass": {"ms_per_launch": sum(x.ms_row_pass for x in kst) / n_rp,
-                            "launches_per_step": n_rp / len(kst)},
-            "k_hub_update": {"ms_per_launch": sum(x.ms_hub_update for x in kst) / n_ep,
-                             "launches_per_step": n_ep / len(kst)},
-            "k_async": {"ms_per_launch": sum(x.ms_tiles for x in kst) / n_ep, "launches_per_step": n_ep / len(kst)},
-        }
-        tot = sum(v["ms_per_launch"] * v["launches_per_step"] for v in kernels.values())
-        for v in kernels.values():
-            v["share_of_epochs"] = v["ms_per_launch"] * v["launches_per_step"] / tot
     b_epoch = algorithmic_bytes(dims.n_struct, dims.nnz_struct, dims.m)
     peak, peak_src = load_peaks()
     achieved = b_epoch / (ep_med / 1e3) / 1e9
+
+    # the same workload under the hub-lag throughput variant (R-22) and under STEP_LJ
+    # (SURVEY A-4): 20 epochs each on the same LP, timed per epoch (not the headline)
+    variants = {}
+    if not args.no_variants:
+        for name, mode, rule in (("hublag_lmax", th.THETIS_MODE_ASYNC_HUBLAG, th.THETIS_STEP_LMAX),
+                                 ("async_lj", th.THETIS_MODE_ASYNC, th.THETIS_STEP_LJ)):
+            rec = {}
+            step(src.data_ptr(), dst.data_ptr(), w.data_ptr(), sel.data_ptr(), rec, mode=mode, rule=rule)
+            x = rec["st"]
+            med = statistics.median(list(x.ms_per_epoch)[:EPOCHS])
+            v = {"mode": mode, "step_rule": rule, "epoch_ms_median": med,
+                 "updates_per_s": x.coordinate_updates / EPOCHS / (med / 1e3),
+                 "GBps": b_epoch / (med / 1e3) / 1e9, "frac": b_epoch / (med / 1e3) / 1e9 / peak,
+                 "f_beta": rec["ob"].f_beta, "lp_obj": rec["ob"].lp_obj,
+                 "max_violation_eps": rec["ob"].max_violation_eps, "cover_cost": rec["rr"].cost}
+            if x.row_pass_launches:
+                ne = min(int(x.epochs), 64)
+                v["kernels_ms_per_launch"] = {"k_rows_pass": x.ms_row_pass / x.row_pass_launches,
+                                              "k_hub_update": x.ms_hub_update / ne, "k_async": x.ms_tiles / ne}
+            variants[name] = v
 
     # end to end through the C ABI with host buffers (pinned), H2D + D2H inside
     e2e = None
@@ -316,7 +331,8 @@ def run_thetis(args):
         "data": "synthetic (R-MAT generated on device from seed; BASELINE configs[4])",
         "config": {"workload": f"{CFG_NAME}: VC LP of R-MAT scale {p['scale']} ({E} edge samples, a,b,c = "
                                f"{p['a']},{p['b']},{p['c']}), weights U[1,10), beta {BETA}, {EPOCHS} async "
-                               "epochs (STEP_LMAX), VC_HALF rounding",
+                               "epochs (THETIS_MODE_ASYNC: Alg. 1's permuted sweep, Hogwild; STEP_LMAX), VC_HALF "
+                               "rounding",
                    "step": "build + 20 SCD epochs + reductions + rounding",
                    "vertices": n, "unique_edges_rows": int(dims.m), "coordinates": int(dims.N),
                    "nnz_struct": int(dims.nnz_struct), "l2": "inputs (8.6 GB edge list) and state exceed the L2",
@@ -326,12 +342,21 @@ def run_thetis(args):
                   "GBps": achieved, "frac_of_8TBps_nominal": achieved / 8000.0},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(),
-                     "kernel": "one SCD epoch = k_rows_pass + k_hub_update + k_async (CUDA events around each "
-                               "epoch on the launching stream; SURVEY 8(d) bytes per epoch)", "peak_source": peak_src,
-                     "kernels": kernels},
+                     "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of "
+                                       "one k_async_pi launch (ncu --set full on this command), not measured in "
+                                       "this run",
+                     "kernel": "k_async_pi: one SCD epoch of THETIS_MODE_ASYNC (one launch per epoch; CUDA events "
+                               "around each epoch on the launching stream; SURVEY 8(d) bytes per epoch)",
+                     "peak_source": peak_src},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),
                    "selected": int(rr.n_selected)},
+        "progress": {"f_beta_start": info["ob0"].f_beta if "ob0" in info else None, "f_beta_end": ob.f_beta,
+                     "eps_start": info["ob0"].max_violation_eps if "ob0" in info else None,
+                     "eps_end": ob.max_violation_eps,
+                     "note": "20 epochs of Alg. 1 with 1/L_max (Eq. 7) on R-MAT: L_max ~ beta * max degree, so "
+                             "steps are small; variants.async_lj shows the same epochs with 1/L_j"},
+        "variants": variants or None,
         "e2e": e2e,
         "gpu_launches": launches * args.steps if launches is not None else None,
         "clocks": clocks,
@@ -364,7 +389,7 @@ def oracle_step(sample):
     t0 = time.perf_counter()
     lp = oracle.RefLP.graph(oracle.PROB_VC, n, src, dst, vertex_w=w)
     t1 = time.perf_counter()
-    st = lp.solve(BETA, EPOCHS, mode=oracle.MODE_TILE_SYNC, seed=75, step_rule=oracle.STEP_LMAX)
+    st = lp.solve(BETA, EPOCHS, mode=oracle.MODE_ASYNC, seed=75, step_rule=oracle.STEP_LMAX)
     t2 = time.perf_counter()
     lp.objective(BETA)
     lp.round(oracle.ROUND_VC_HALF)
@@ -383,15 +408,51 @@ def ref_sample():
 
 
 SAMPLE_DESC = (f"the same recipe at R-MAT scale {REF_SAMPLE_SCALE} ({1 << REF_SAMPLE_SCALE} vertices, "
-               f"{16 << REF_SAMPLE_SCALE} samples): build + {EPOCHS} epochs (async reference trajectory) + "
-               "reductions + rounding, oracle fp64, single thread")
+               f"{16 << REF_SAMPLE_SCALE} samples): build + {EPOCHS} epochs of Alg. 1 in the permuted order "
+               "(oracle MODE_ASYNC, the async reference trajectory) + reductions + rounding, oracle fp64, "
+               "one thread pinned to one core")
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class PinnedCore:
+    """Run the oracle on one host core (SURVEY §8(d) "Timing, oracle": taskset -c 0 equivalent)."""
+
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = min(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *a):
+        if self.prev:
+            os.sched_setaffinity(0, self.prev)
+
+
+def host_info(core):
+    return {"cpu_model": cpu_model(), "pinned_core": core, "host_cores": os.cpu_count(),
+            "threads_used": "1 of %s cores" % os.cpu_count()}
 
 
 def cpu_baseline():
     sample = ref_sample()
-    upd, t, t_ep = oracle_step(sample)
+    with PinnedCore() as pc:
+        upd, t, t_ep = oracle_step(sample)
     return {"value": upd / t, "unit": "coordinate updates/s", "cores": 1, "kind": "oracle",
-            "sample": SAMPLE_DESC, "epoch_updates_per_s": upd / t_ep, "seconds": t}
+            "sample": SAMPLE_DESC, "epoch_updates_per_s": upd / t_ep, "seconds": t, **host_info(pc.core)}
 
 
 def run_reference(args):
@@ -399,13 +460,14 @@ def run_reference(args):
     if rank != 0:
         return
     sample = ref_sample()
-    for _ in range(args.warmup):
-        oracle_step(sample)
     tot_t, tot_u = 0.0, 0
-    for _ in range(args.steps):
-        u, t, _ = oracle_step(sample)
-        tot_t += t
-        tot_u += u
+    with PinnedCore() as pc:
+        for _ in range(args.warmup):
+            oracle_step(sample)
+        for _ in range(args.steps):
+            u, t, _ = oracle_step(sample)
+            tot_t += t
+            tot_u += u
     v = tot_u / tot_t
     out = {"metric": METRIC, "value": v, "unit": "coordinate updates/s", "n_gpus": ws_n, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
@@ -413,7 +475,7 @@ def run_reference(args):
            "config": {"workload": f"{CFG_NAME} (bounded CPU sample)", "sample": SAMPLE_DESC},
            "impl": "reference",
            "cpu_baseline": {"value": v, "unit": "coordinate updates/s", "cores": 1, "kind": "oracle",
-                            "sample": SAMPLE_DESC},
+                            "sample": SAMPLE_DESC, **host_info(pc.core)},
            "e2e": {"value": v, "unit": "coordinate updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

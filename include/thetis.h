@@ -67,8 +67,11 @@ typedef enum {
 enum { THETIS_EQ = 0, THETIS_GE = 1, THETIS_LE = 2 };          /* row sense */
 enum { THETIS_MIN = 0, THETIS_MAX = 1 };                       /* objective sense */
 enum { THETIS_PROB_GENERIC = 0, THETIS_PROB_VC = 1, THETIS_PROB_MIS = 2, THETIS_PROB_MWC = 3 };
-enum { THETIS_MODE_DETERMINISTIC = 0, THETIS_MODE_ASYNC = 1,
-       THETIS_MODE_ASYNC_SERIAL = 2 /* diagnostic: the async kernel with one tile in flight */ };
+enum { THETIS_MODE_DETERMINISTIC = 0,
+       THETIS_MODE_ASYNC = 1,        /* Alg. 1's permuted sweep, Hogwild (R-6) */
+       THETIS_MODE_ASYNC_SERIAL = 2, /* diagnostic: the THETIS_MODE_ASYNC kernel with one tile in flight */
+       THETIS_MODE_ASYNC_HUBLAG = 3, /* throughput variant: row pass + lagged hub step (R-22) */
+       THETIS_MODE_ASYNC_HUBLAG_SERIAL = 4 /* diagnostic: the hub-lag kernels with one tile in flight */ };
 enum { THETIS_STEP_LMAX = 0, /* Alg. 1: 1/L_max, Eq. 7 */
        THETIS_STEP_LJ = 1    /* 1/L_j per unit: extension, not the paper's (R-4) */ };
 enum { THETIS_ROUND_VC_HALF = 1,   /* Lemma-1 threshold (1-eps)/2 + fix-up */

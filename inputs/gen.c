@@ -12,7 +12,7 @@
  * SplitMix64 generator seeded with `seed` (Steele, Lea, Flood 2014):
  *     state_i = seed + (i+1)*0x9E3779B97F4A7C15,  out = mix(state_i).
  * inputs/gen_cuda.cu implements the same function on the device for the
- * large bench inputs; tests/test_inputs*.py check the two agree.
+ * large bench inputs; tests/test_inputs.py (its GPU test) checks the two agree.
  */
 #include <math.h>
 #include <stdint.h>

@@ -1,7 +1,7 @@
 // Device twin of inputs/gen.c for the inputs too large to generate on the
 // host inside a bench run (R-MAT scale 26: 1.07e9 edges).  Same counter-based
-// definitions, bit for bit (tests/test_inputs_gpu.py checks it against the
-// host generator).  Holds none of the method's arithmetic.
+// definitions, bit for bit (tests/test_inputs.py::test_device_twin_matches_host checks
+// it against the host generator).  Holds none of the method's arithmetic.
 #include <cstdint>
 #include <cuda_runtime.h>
 

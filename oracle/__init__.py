@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBS: dict = {}
 
 PROB_VC, PROB_MIS, PROB_MWC = 1, 2, 3
-MODE_DET, MODE_ASYNC, MODE_CYCLIC, MODE_TILE_SYNC = 0, 1, 2, 3
+MODE_DET, MODE_ASYNC, MODE_CYCLIC, MODE_HUBLAG_REPLAY, MODE_PI_TILE_SYNC = 0, 1, 2, 3, 4
 STEP_LMAX, STEP_LJ = 0, 1
 ROUND_VC_HALF, ROUND_VC_FIXUP, ROUND_MIS_GREEDY, ROUND_MWC_CKR = 1, 2, 3, 4
 ROUND_SC_THRESHOLD, ROUND_SC_RANDOM, ROUND_MIS_BANSAL = 5, 6, 7

@@ -19,12 +19,13 @@
 #endif
 
 #define GOLDEN 0x9E3779B97F4A7C15ULL
-#define HUB_NNZ 512 /* R-6: tiles whose scalar columns hold more nonzeros are hub tiles */
+#define HUB_NNZ 512 /* R-17 / R-22: tiles whose scalar columns hold more nonzeros are hub tiles (the row
+                         layout and the hub-lag variant; Alg. 1 (mode 1) does not depend on it) */
 
 enum { PROB_GENERIC = 0, PROB_VC = 1, PROB_MIS = 2, PROB_MWC = 3 };
 enum { SENSE_EQ = 0, SENSE_GE = 1, SENSE_LE = 2 };
 enum { OBJ_MIN = 0, OBJ_MAX = 1 };
-enum { MODE_DET = 0, MODE_ASYNC = 1, MODE_CYCLIC = 2 };
+enum { MODE_DET = 0, MODE_ASYNC = 1, MODE_CYCLIC = 2, MODE_HUBLAG_REPLAY = 3, MODE_PI_TILE_SYNC = 4 };
 enum { STEP_LMAX = 0, STEP_LJ = 1 };
 enum { ROUND_VC_HALF = 1, ROUND_VC_FIXUP = 2, ROUND_MIS_GREEDY = 3, ROUND_MWC_CKR = 4, ROUND_SC_THRESHOLD = 5,
        ROUND_SC_RANDOM = 6, ROUND_MIS_BANSAL = 7 };
@@ -830,7 +831,7 @@ static int64_t step_tile_sync(ref_lp* lp, const step_ctx* s, int64_t u0, int64_t
 
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                      ref_stats* st) {
-    if (!(beta > 0) || epochs < 0 || mode < 0 || mode > 3 || step_rule < 0 || step_rule > 1)
+    if (!(beta > 0) || epochs < 0 || mode < 0 || mode > 4 || step_rule < 0 || step_rule > 1)
         return REF_INVALID_ARG;
     step_ctx s = make_ctx(lp, beta, step_rule);
     if (lp->ubar) recompute_ua(lp);
@@ -850,14 +851,14 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
     int64_t n_tiles = (lp->U + 31) / 32;
     const int64_t n_struct_units = lp->n_blocks + lp->n_scalar;
     const int64_t n_struct_tiles = (n_struct_units + 31) / 32;
-    int64_t* perm = (mode == MODE_ASYNC || mode >= 3) ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
+    int64_t* perm = mode != MODE_DET && mode != MODE_CYCLIC ? (int64_t*)xcalloc(n_tiles, sizeof(int64_t)) : NULL;
     /* hub tiles of the async reference (R-6): VC / MIS tiles whose scalar
      * columns hold more than HUB_NNZ nonzeros */
     uint8_t* hub_tile = NULL;
     int64_t* hub_cols = NULL;
     REAL* hub_new = NULL;
     int64_t n_hub_cols = 0;
-    if (mode >= 3 && (lp->problem == PROB_VC || lp->problem == PROB_MIS)) {
+    if (mode == MODE_HUBLAG_REPLAY && (lp->problem == PROB_VC || lp->problem == PROB_MIS)) {
         hub_tile = (uint8_t*)xcalloc(n_struct_tiles, 1);
         hub_cols = (int64_t*)xcalloc(n_struct_tiles * 32, sizeof(int64_t));
         for (int64_t t = 0; t < n_struct_tiles; t++) {
@@ -888,7 +889,28 @@ int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed
                     nnz += step_unit(lp, &s, u);
                     updates += c;
                 }
-        } else if (mode == 3) {
+        } else if (mode == MODE_PI_TILE_SYNC) {
+            /* the permuted sweep of MODE_ASYNC, a tile's units in three groups: its
+             * k-blocks one at a time, then its scalar columns synchronously (all take
+             * their steps from the state at that point, then apply in unit order), then
+             * its slacks synchronously (the THETIS_MODE_ASYNC kernel with one tile in
+             * flight; test reference for its arithmetic) */
+            REAL nv[32 * 64];
+            thetis_ref_tile_perm(n_tiles, seed, e, perm);
+            for (int64_t t = 0; t < n_tiles; t++) {
+                int64_t u0 = perm[t] * 32, u1 = u0 + 32 < lp->U ? u0 + 32 : lp->U;
+                /* k-blocks one at a time (as in mode 1), then the scalar columns
+                 * synchronously, then the slacks synchronously */
+                for (; u0 < u1 && u0 < lp->n_blocks; u0++) {
+                    if (unit_fixed(lp, u0)) continue;
+                    nnz += step_unit(lp, &s, u0);
+                    updates += lp->block_k;
+                }
+                int64_t us = u0 < n_struct_units ? (u1 < n_struct_units ? u1 : n_struct_units) : u0;
+                nnz += step_tile_sync(lp, &s, u0, us, &updates, nv);
+                nnz += step_tile_sync(lp, &s, us, u1, &updates, nv);
+            }
+        } else if (mode == MODE_HUBLAG_REPLAY) {
             REAL nv[32 * 64];
             /* (1) the row pass: the pending hub steps of the previous epoch enter r
              * (none in the first), then every slack takes its step (slacks share no

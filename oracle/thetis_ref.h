@@ -93,19 +93,28 @@ int thetis_ref_step_unit(ref_lp* lp, float beta, int64_t u, int step_rule);
 double thetis_ref_grad(const ref_lp* lp, float beta, int64_t j);
 
 /* mode 0 = deterministic coloured sweep (R-5);
- * mode 1 = unit-sequential replay of the tile permutation (Alg. 1 one
- *          coordinate at a time, in the async order);
+ * mode 1 = Alg. 1 one unit at a time in the permuted order: tiles
+ *          of 32 consecutive units (blocks, scalars, slacks) in the order pi_e,
+ *          units of a tile ascending -- THE ASYNC REFERENCE TRAJECTORY (R-6):
+ *          the GPU's THETIS_MODE_ASYNC is compared against it within the
+ *          BASELINE tolerances;
  * mode 2 = plain cyclic sweep;
- * mode 3 = the async reference trajectory (R-6), per epoch: (1) the hub
- *          steps pending from the previous epoch enter r, then every slack
- *          takes its step (slacks share no row); (2) VC / MIS: the scalar
- *          columns of the hub tiles (tiles of 32 structural units whose columns
- *          hold > 512 nonzeros) take one synchronous step, z moves and the
- *          step d stays pending; (3) the tiles of 32 structural units in
- *          permutation order (pi_e over the structural tiles), each one
- *          synchronous step of its units (every unit steps from the state at
- *          the tile's start; r without the pending d), hub tiles skipped.
- *          After the call's last epoch d enters r (r = A z - b on return). */
+ * mode 3 = replay of the hub-lag schedule (R-22, THETIS_MODE_ASYNC_HUBLAG), per
+ *          epoch: (1) the hub steps pending from the previous epoch enter r,
+ *          then every slack takes its step (slacks share no row); (2) VC / MIS:
+ *          the scalar columns of the hub tiles (tiles of 32 structural units
+ *          whose columns hold > 512 nonzeros, R-22's definition) take one
+ *          synchronous step, z moves and the step d stays pending; (3) the tiles
+ *          of 32 structural units in permutation order (pi_e over the structural
+ *          tiles), each one synchronous step of its units (every unit steps from
+ *          the state at the tile's start; r without the pending d), hub tiles
+ *          skipped.  After the call's last epoch d enters r (r = A z - b on
+ *          return).  Exact-arithmetic reference of THETIS_MODE_ASYNC_HUBLAG_SERIAL;
+ *          a different algorithm from mode 1 with the same fixed point x(beta);
+ * mode 4 = mode 1's order with each tile's units in three groups: its k-blocks one
+ *          at a time (as in mode 1), then its scalar columns synchronously (all step
+ *          from the same state, then apply in unit order), then its slacks likewise:
+ *          the exact-arithmetic reference of THETIS_MODE_ASYNC_SERIAL. */
 int thetis_ref_solve(ref_lp* lp, float beta, int epochs, int mode, uint64_t seed,
                      int step_rule, ref_stats* st);
 int thetis_ref_objective(const ref_lp* lp, float beta, ref_objective* out);

@@ -34,6 +34,7 @@ THETIS_EQ, THETIS_GE, THETIS_LE = 0, 1, 2
 THETIS_MIN, THETIS_MAX = 0, 1
 THETIS_PROB_GENERIC, THETIS_PROB_VC, THETIS_PROB_MIS, THETIS_PROB_MWC = 0, 1, 2, 3
 THETIS_MODE_DETERMINISTIC, THETIS_MODE_ASYNC, THETIS_MODE_ASYNC_SERIAL = 0, 1, 2
+THETIS_MODE_ASYNC_HUBLAG, THETIS_MODE_ASYNC_HUBLAG_SERIAL = 3, 4
 THETIS_STEP_LMAX, THETIS_STEP_LJ = 0, 1
 THETIS_ROUND_VC_HALF, THETIS_ROUND_VC_FIXUP, THETIS_ROUND_MIS_GREEDY, THETIS_ROUND_MWC_CKR = 1, 2, 3, 4
 THETIS_ROUND_SC_THRESHOLD, THETIS_ROUND_SC_RANDOM, THETIS_ROUND_MIS_BANSAL = 5, 6, 7

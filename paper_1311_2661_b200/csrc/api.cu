@@ -114,6 +114,7 @@ THETIS_API int thetis_build_graph_lp(thetis_lp** out, void* workspace, size_t ws
                                      int64_t n, int64_t n_edges, const int32_t* src, const int32_t* dst,
                                      const float* vertex_w, const float* edge_w, int k, const int32_t* terminals,
                                      int t_per_label) {
+    thetis::NvtxRange nvtx_("thetis_build_graph_lp");
     if (!out) return fail_global(THETIS_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     size_t need = 0;
@@ -152,6 +153,7 @@ THETIS_API int thetis_build_lp(thetis_lp** out, void* workspace, size_t ws_bytes
                                const int64_t* csr_rowptr, const int32_t* csr_colidx, const float* csr_val,
                                const float* b, const float* c, const int8_t* sense, const float* lo, const float* hi,
                                int obj_sense, int block_k, int64_t n_blocks) {
+    thetis::NvtxRange nvtx_("thetis_build_lp");
     if (!out) return fail_global(THETIS_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     size_t need = 0;
@@ -223,9 +225,10 @@ THETIS_API int thetis_get_r(const thetis_lp* lp, float* dst, int64_t count) {
 
 THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                             thetis_solve_stats* stats) {
+    thetis::NvtxRange nvtx_("thetis_solve");
     if (!lp) return THETIS_ERR_INVALID_ARG;
     if (!(beta > 0.0f) || !isfinite(beta) || epochs < 0 ||
-        (mode != THETIS_MODE_DETERMINISTIC && mode != THETIS_MODE_ASYNC && mode != THETIS_MODE_ASYNC_SERIAL) ||
+        (mode < THETIS_MODE_DETERMINISTIC || mode > THETIS_MODE_ASYNC_HUBLAG_SERIAL) ||
         (step_rule != THETIS_STEP_LMAX && step_rule != THETIS_STEP_LJ))
         return set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments to thetis_solve");
     if (lp->anchors) THETIS_TRY(recompute_ua(lp));
@@ -240,11 +243,12 @@ THETIS_API int thetis_solve(thetis_lp* lp, float beta, int epochs, int mode, uin
 THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float beta0, float beta_growth,
                                 int max_outer, int inner_epochs, int mode, uint64_t seed, int step_rule,
                                 double target_eps, thetis_alm_stats* stats) {
+    thetis::NvtxRange nvtx_("thetis_solve_alm");
     if (!lp) return THETIS_ERR_INVALID_ARG;
     if (!ubar || !zbar || !is_device_ptr(ubar) || !is_device_ptr(zbar) || !(beta0 > 0.0f) || !isfinite(beta0) ||
         !(beta_growth >= 1.0f) || !isfinite(beta_growth) || max_outer < 1 || max_outer > THETIS_MAX_ALM_ROUNDS ||
         inner_epochs < 0 ||
-        (mode != THETIS_MODE_DETERMINISTIC && mode != THETIS_MODE_ASYNC && mode != THETIS_MODE_ASYNC_SERIAL) ||
+        (mode < THETIS_MODE_DETERMINISTIC || mode > THETIS_MODE_ASYNC_HUBLAG_SERIAL) ||
         (step_rule != THETIS_STEP_LMAX && step_rule != THETIS_STEP_LJ))
         return set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments to thetis_solve_alm");
     THETIS_TRY(thetis_set_anchors(lp, zbar, ubar));
@@ -275,12 +279,14 @@ THETIS_API int thetis_solve_alm(thetis_lp* lp, float* ubar, float* zbar, float b
 }
 
 THETIS_API int thetis_objective(thetis_lp* lp, float beta, thetis_objective_t* out) {
+    thetis::NvtxRange nvtx_("thetis_objective");
     if (!lp || !out || !(beta > 0.0f)) return lp ? set_error(lp, THETIS_ERR_INVALID_ARG, "bad arguments") : THETIS_ERR_INVALID_ARG;
     return objective(lp, beta, out);
 }
 
 THETIS_API int thetis_round_x(thetis_lp* lp, const float* x, int rule, uint64_t seed, int reps, uint8_t* out_assign,
                               thetis_round_result* out) {
+    thetis::NvtxRange nvtx_("thetis_round_x");
     if (!lp || !x || !out) return THETIS_ERR_INVALID_ARG;
     const float* xd = x;
     if (!is_device_ptr(x)) {
@@ -294,6 +300,7 @@ THETIS_API int thetis_round_x(thetis_lp* lp, const float* x, int rule, uint64_t 
 
 THETIS_API int thetis_round(thetis_lp* lp, int rule, uint64_t seed, int reps, uint8_t* out_assign,
                             thetis_round_result* out) {
+    thetis::NvtxRange nvtx_("thetis_round");
     if (!lp || !out) return THETIS_ERR_INVALID_ARG;
     return round_x(lp, lp->d.z, rule, seed, reps, out_assign, out);
 }

@@ -1,0 +1,644 @@
+// THETIS_MODE_ASYNC: Alg. 1 on f_beta (Eq. 5), run Hogwild-style
+// (many updaters share x, "each thread runs Alg. 1") in the order of the
+// oracle's sequential reference trajectory (R-6):
+//
+//   units  = k-blocks, scalar structural columns, slacks (ids in that order);
+//   tiles  = 32 consecutive unit ids, n_tiles = ceil(U / 32);
+//   epoch e visits the tiles in the order pi_e (4-round Feistel keyed by
+//            (seed, e), thetis_internal.cuh), every unit once.
+//
+// The GPU hands out the permuted positions in order and runs a small window of them
+// concurrently.  Inside a tile, k-blocks step one at a time (neighbouring MWC vertices
+// share rows), then the scalar columns synchronously (all read r, then all write it with
+// red.global.add.f32, so no update is lost), then the slacks likewise; tiles in flight
+// read r stale by at most the window.  With one worker (THETIS_MODE_ASYNC_SERIAL) this is exactly the
+// replay of oracle mode 4.
+//
+// Big tiles (scalar columns holding more than kJobMin nonzeros: power-law hubs) are
+// cut into chunks of kJobChunk nonzeros that many warps process: per epoch the
+// sequence of positions is expanded into *slots* -- a big tile at position p becomes
+// its gather chunks (partial column dots added into the tile's accumulators; the last
+// one takes the tile's steps), and its scatter chunks are inserted G positions later
+// (G = a quarter of the window; a scatter drawn before its tile's steps are known is
+// kept by its warp and run as soon as they are).
+// A hub is thus gathered at its position within microseconds by many warps and its
+// step reaches r G positions later: a bounded delay, the async model of P:463-476.
+//
+// Work distribution: slot batches of kPiBatch; batch b belongs to CTA b mod gridDim,
+// whose warps draw that CTA's batches in order from a shared-memory counter, so all
+// CTAs sweep the slots together without a global atomic per tile, and the slots in
+// flight are ~ (warps in the grid) x kPiBatch consecutive ones.
+#include <cub/cub.cuh>
+
+#include "scd_device.cuh"
+
+namespace thetis {
+namespace {
+
+constexpr int kPiWarps = 8;           // warps per CTA
+constexpr int kPiBatch = 4;           // consecutive slots a warp draws at once
+constexpr int64_t kJobChunk = 2048;   // nonzeros per big-tile chunk
+constexpr int64_t kJobMin = 4096;     // a tile whose scalar range holds more is big
+constexpr int kVShift = 7;            // slot index: one entry per 128 slots
+
+// one big tile (static per solve) and its per-epoch state
+struct PiJob {
+    int64_t tile, cb, ce;             // tile, its scalar CSC range [cb, ce)
+    int32_t n_chunks;
+    int32_t gdone;                    // gather chunks finished this epoch
+    uint32_t ready;                   // = stamp once d[] holds this epoch's steps
+    int32_t pad[3];
+    float acc[32];                    // column dots D_j (device-scope atomics)
+    float d[32];                      // steps of the tile's columns
+};
+
+// scatter chunks whose tile's steps were not ready when drawn: kept per warp and run
+// as soon as they are (a warp never waits while it has other slots to run)
+constexpr int kDefer = 8;
+struct Deferred {
+    int32_t b[kDefer], c[kDefer];
+    int n;
+};
+
+struct PiCtx {
+    PermKeys K;                       // pi_e on [0, n_tiles)
+    int64_t n_tiles;
+    int64_t n_struct;                 // structural units n_blocks + n_scalar
+    PiJob* jobs;
+    int64_t n_ev;                     // events (2 per big tile), sorted by (position, kind)
+    const int64_t* ev_pos;            // position the event sits at
+    const int64_t* ev_vstart;         // its first slot
+    const int32_t* ev_val;            // 2 b + kind (kind 1 = gathers of big tile b, 0 = scatters)
+    const int32_t* vindex;            // per 2^kVShift slots: last event starting at or before, or -1
+    const int64_t* n_slots;           // slots this epoch (device)
+    uint32_t stamp;                   // epoch stamp of the call (1, 2, ...)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {  // polls: no L1 invalidation
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_release(int32_t* p, int v) {
+    int old;
+    asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// the tile's scalar columns: lanes [a, b), first column j0
+__device__ __forceinline__ TileCols tile_cols(const DevLP& L, int64_t tile) {
+    TileCols tc;
+    tc.u0 = tile * 32;
+    int b;
+    scalar_lanes(L, tc.u0, tc.a, b);
+    tc.ncols = b - tc.a;
+    tc.j0 = L.n_blocks * L.k + (tc.u0 + tc.a - L.n_blocks);
+    return tc;
+}
+// column starts of the tile's scalar range into sm.cp (cp[ncols] = end)
+__device__ __forceinline__ void load_cp(const DevLP& L, const TileCols& tc, WarpSmem& sm, int lane) {
+    if (lane < tc.ncols) sm.cp[lane] = L.colptr[tc.j0 + lane];
+    if (lane == 0) sm.cp[tc.ncols] = L.colptr[tc.j0 + tc.ncols];
+    __syncwarp();
+}
+
+// slack lanes of a tile: new value from r_i (gather side); returns the change of r_i
+__device__ __forceinline__ float slack_lane_gather(const DevLP& L, const StepParams& P, int64_t q, int64_t& row) {
+    row = slack_row_of(L, q);
+    const int64_t j = L.n_s + q;
+    const float sig = row_sigma(L, row);
+    const float rv = ld_cg(L.r + row);
+    const float z = L.z[j];
+    const float zn = slack_new<true>(L, P, row, j, sig, rv, z);
+    L.z[j] = zn;
+    const float d = __fsub_rn(zn, z);
+    return sig < 0.0f ? -d : d;
+}
+
+// ---- k-blocks (MWC vertex blocks, App. E): one block at a time in unit order, each by
+// the whole warp (neighbouring vertices share rows, so a tile-synchronous step of
+// coupled blocks would leave Alg. 1's sequential trajectory).  The block's k columns
+// are one contiguous CSC range; lane q takes entries q, q + 32, ... of it.
+template <int KC>
+__device__ void block_step_warp(const DevLP& L, const StepParams& P, int64_t u, WarpSmem& sm, int lane) {
+    const int k = L.k;
+    const int64_t f = u * k;
+    if (lane <= k) sm.cp[lane] = L.colptr[f + lane];
+    float zl = 0.0f, cl = 0.0f, ul = 0.0f, zbl = 0.0f;
+    double nrm = 0.0;
+    if (lane < k) {
+        zl = L.z[f + lane];
+        cl = c_int(L, f + lane);
+        ul = ua_of(L, f + lane);
+        zbl = zbar_of(L, f + lane);
+        nrm = col_norm2(L, f + lane);
+        sm.acc[lane] = 0.0f;
+    }
+    __syncwarp();
+    const int64_t cb = sm.cp[0], ce = sm.cp[k];
+    // D_l = a_l^T r: lane q adds its entries into its column's slot
+    for (int64_t t0 = cb; t0 < ce; t0 += 64) {
+        uint32_t raw[2];
+        float v[2];
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const int64_t t = t0 + lane + 32 * e;
+            raw[e] = t < ce ? (uint32_t)L.rowidx[t] : 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const int64_t t = t0 + lane + 32 * e;
+            v[e] = 0.0f;
+            if (t < ce) {
+                const float rv = ld_cg(L.r + (raw[e] & kRowMask));
+                v[e] = L.val ? L.val[t] * rv : ((raw[e] & kSignBit) ? -rv : rv);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const int64_t t = t0 + lane + 32 * e;
+            if (t < ce && v[e] != 0.0f) atomicAdd(&sm.acc[col_of(sm, k, t)], v[e]);
+        }
+    }
+    __syncwarp();
+    // step: y_l = z_l - g_l / L (L_max, or the block's largest L_j), projection on the simplex
+    double mx = nrm;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double q = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = q > mx ? q : mx;
+    }
+    const float invL = unit_invL(P, mx);
+    const float Dl = lane < k ? sm.acc[lane] : 0.0f;
+    const float yl = __fsub_rn(zl, __fmul_rn(grad_fast(cl, ul, Dl, zl, zbl, P.beta, P.inv_beta), invL));
+    float y[KC], x[KC];
+#pragma unroll
+    for (int l = 0; l < KC; l++) y[l] = __shfl_sync(0xffffffffu, yl, l & 31);
+    project_simplex<KC>(y, k, x);
+    float xl = 0.0f;
+#pragma unroll
+    for (int l = 0; l < KC; l++)
+        if (l == lane) xl = x[l];
+    if (lane < k) {
+        sm.d[lane] = __fsub_rn(xl, zl);
+        L.z[f + lane] = xl;
+    }
+    __syncwarp();
+    // scatter: r_i += a_ij d_col
+    for (int64_t t = cb + lane; t < ce; t += 32) {
+        const float d = sm.d[col_of(sm, k, t)];
+        const uint32_t rw = (uint32_t)L.rowidx[t];
+        if (d != 0.0f) red_add(L.r + (rw & kRowMask), L.val ? __fmul_rn(L.val[t], d) : ((rw & kSignBit) ? -d : d));
+    }
+    __syncwarp();  // the next block's loads come after these (same-warp ordering)
+}
+
+// ---- one tile.  scalars = false: the scalar columns are a big tile's (done by chunks)
+template <bool kBlocks, int KC>
+__device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx& C, int64_t tile, WarpSmem& sm,
+                                int lane, bool scalars) {
+    const int64_t u = tile * 32 + lane;
+    if (tile * 32 >= C.n_struct) {  // slack tile
+        float dr = 0.0f;
+        int64_t row = 0;
+        if (u < L.U) dr = slack_lane_gather(L, P, u - C.n_struct, row);
+        if (dr != 0.0f) red_add(L.r + row, dr);
+        return;
+    }
+    // k-blocks of the tile: one at a time, in unit order (Alg. 1's order inside the tile)
+    if (kBlocks && tile * 32 < L.n_blocks) {
+        const int nb = (int)(L.n_blocks - tile * 32 < 32 ? L.n_blocks - tile * 32 : 32);
+        unsigned live = __ballot_sync(0xffffffffu, lane < nb && !(L.unit_fixed && L.unit_fixed[u]));
+        while (live) {
+            const int i = __ffs(live) - 1;
+            live &= live - 1;
+            block_step_warp<KC>(L, P, tile * 32 + i, sm, lane);
+        }
+    }
+    // then the tile's scalar columns synchronously (all read r before any write), then its
+    // slacks (a tile mixing both is the one at the structural / slack boundary)
+    const TileCols tc = tile_cols(L, tile);
+    bool lane_path = false;
+    int64_t beg = 0, end = 0, cb = 0, ce = 0;
+    unsigned moved = 0;
+    if (tc.ncols > 0 && scalars) {
+        load_cp(L, tc, sm, lane);
+        beg = sm.cp[0];
+        end = sm.cp[tc.ncols];
+        const int cl = lane - tc.a;  // this lane's scalar column, if any
+        if (cl >= 0 && cl < tc.ncols) {
+            cb = sm.cp[cl];
+            ce = sm.cp[cl + 1];
+        }
+        lane_path = __reduce_max_sync(0xffffffffu, (unsigned)(ce - cb)) <= 48u;
+        float z = 0.0f, cj = 0.0f;
+        if (cl >= 0 && cl < tc.ncols) {
+            z = L.z[tc.j0 + cl];
+            cj = c_int(L, tc.j0 + cl);
+        }
+        // scalar_step indexes lanes 0..ncols-1 = columns: shuffle the column's data there
+        z = __shfl_sync(0xffffffffu, z, (lane + tc.a) & 31);
+        cj = __shfl_sync(0xffffffffu, cj, (lane + tc.a) & 31);
+        float D = 0.0f;
+        if (lane_path) {  // one lane per column, eight loads in flight
+            for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+                uint32_t raw[8];
+                float rv[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) raw[q] = q0 + q < ce ? (uint32_t)L.rowidx[q0 + q] : 0u;
+#pragma unroll
+                for (int q = 0; q < 8; q++) rv[q] = q0 + q < ce ? ld_cg(L.r + (raw[q] & kRowMask)) : 0.0f;
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    if (q0 + q < ce) D += L.val ? L.val[q0 + q] * rv[q] : ((raw[q] & kSignBit) ? -rv[q] : rv[q]);
+            }
+            D = __shfl_sync(0xffffffffu, D, (lane + tc.a) & 31);
+        } else {  // the warp walks the tile's CSC range coalesced
+            sm.acc[lane] = 0.0f;
+            __syncwarp();
+            gather_range(L, sm, tc.ncols, beg, end, lane, 0);
+            D = sm.acc[lane];
+        }
+        const float d = scalar_step(L, P, tc, D, lane, z, cj);  // lane = column index
+        sm.d[lane] = d;
+        moved = __ballot_sync(0xffffffffu, d != 0.0f);
+    }
+    __syncwarp();
+    // scatters
+    if (moved) {
+        if (lane_path) {
+            const int cl = lane - tc.a;
+            const float d = cl >= 0 && cl < 32 ? sm.d[cl] : 0.0f;
+            if (d != 0.0f)
+                for (int64_t q = cb; q < ce; q++) {
+                    const uint32_t raw = (uint32_t)L.rowidx[q];
+                    const float a = entry_val(L, q, raw);
+                    red_add(L.r + (raw & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
+                }
+        } else {
+            scatter_range(L, sm, tc.ncols, beg, end, lane, 0);
+        }
+    }
+    __syncwarp();  // the slacks' loads come after the scalars' writes (same-warp ordering)
+    if (u >= C.n_struct && u < L.U) {
+        int64_t srow = 0;
+        const float dr = slack_lane_gather(L, P, u - C.n_struct, srow);
+        if (dr != 0.0f) red_add(L.r + srow, dr);
+    }
+    __syncwarp();
+}
+
+// ---- big tiles
+// gather chunk c of big tile b: partial dots of its columns over the chunk; the last
+// one takes the tile's steps (tile-synchronous) and marks them ready
+template <bool kBlocks, int KC>
+__device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, int32_t b, int c, WarpSmem& sm,
+                           int lane) {
+    PiJob& J = C.jobs[b];
+    if (c == 0) process_tile_pi<kBlocks, KC>(L, P, C, J.tile, sm, lane, false);  // its other units
+    const TileCols tc = tile_cols(L, J.tile);
+    load_cp(L, tc, sm, lane);
+    sm.acc[lane] = 0.0f;
+    __syncwarp();
+    const int64_t c0 = J.cb + (int64_t)c * kJobChunk;
+    const int64_t c1 = c0 + kJobChunk < J.ce ? c0 + kJobChunk : J.ce;
+    gather_range(L, sm, tc.ncols, c0, c1, lane, 0);
+    if (lane < tc.ncols && sm.acc[lane] != 0.0f) atomicAdd(&J.acc[lane], sm.acc[lane]);
+    __syncwarp();  // (the warp barrier orders every lane's partial before lane 0's release)
+    int g = 0;
+    if (lane == 0) g = atom_add_release(&J.gdone, 1);  // orders this chunk's partials before it
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g != J.n_chunks - 1) return;
+    if (lane == 0) (void)ld_acquire_u32((const uint32_t*)&J.gdone);  // every partial is in
+    __syncwarp();
+    const float D = ld_cg(&J.acc[lane]);
+    float z = 0.0f, cj = 0.0f;
+    if (lane < tc.ncols) {
+        z = L.z[tc.j0 + lane];
+        cj = c_int(L, tc.j0 + lane);
+    }
+    J.d[lane] = scalar_step(L, P, tc, D, lane, z, cj);
+    __syncwarp();
+    if (lane == 0) st_release_u32(&J.ready, C.stamp);
+}
+// scatter chunk c of big tile b, whose steps are ready
+__device__ void job_scatter(const DevLP& L, const PiCtx& C, int32_t b, int c, WarpSmem& sm, int lane) {
+    const PiJob& J = C.jobs[b];
+    if (lane == 0) (void)ld_acquire_u32(&J.ready);  // the steps and z written before `ready`
+    __syncwarp();
+    const float d = ld_cg(&J.d[lane]);
+    if (!__any_sync(0xffffffffu, d != 0.0f)) return;
+    const TileCols tc = tile_cols(L, J.tile);
+    load_cp(L, tc, sm, lane);
+    sm.d[lane] = d;
+    __syncwarp();
+    const int64_t c0 = J.cb + (int64_t)c * kJobChunk;
+    const int64_t c1 = c0 + kJobChunk < J.ce ? c0 + kJobChunk : J.ce;
+    scatter_range(L, sm, tc.ncols, c0, c1, lane, 0);
+}
+__device__ __forceinline__ bool job_ready(const PiCtx& C, int32_t b, int lane) {
+    int ok = 0;
+    if (lane == 0) ok = ld_relaxed_u32(&C.jobs[b].ready) == C.stamp;
+    return __shfl_sync(0xffffffffu, ok, 0);
+}
+// run the deferred scatters that are ready (all of them, waiting, when `drain`)
+__device__ void run_deferred(const DevLP& L, const PiCtx& C, Deferred& df, WarpSmem& sm, int lane, bool drain) {
+    int i = 0;
+    while (i < df.n) {
+        if (job_ready(C, df.b[i], lane)) {
+            job_scatter(L, C, df.b[i], df.c[i], sm, lane);
+            __syncwarp();
+            if (lane == 0) {
+                df.b[i] = df.b[df.n - 1];
+                df.c[i] = df.c[df.n - 1];
+                df.n--;
+            }
+            __syncwarp();
+        } else if (drain) {
+            __nanosleep(256);
+        } else {
+            i++;
+        }
+    }
+}
+
+// slot v -> a plain position (returns the tile, kind = 2) or a chunk of an event
+// (kind 1 = gather, 0 = scatter; b = big tile, c = chunk)
+__device__ __forceinline__ int64_t resolve_slot(const PiCtx& C, int64_t v, int& kind, int32_t& b, int& c) {
+    int64_t e = C.n_ev ? C.vindex[v >> kVShift] : -1;
+    while (e + 1 < C.n_ev && C.ev_vstart[e + 1] <= v) e++;
+    int64_t p = v;
+    if (e >= 0) {
+        const int32_t val = C.ev_val[e];
+        const int k = val & 1;
+        b = val >> 1;
+        const int64_t vs = C.ev_vstart[e], n = C.jobs[b].n_chunks;
+        if (v < vs + n) {
+            kind = k;
+            c = (int)(v - vs);
+            return -1;
+        }
+        p = C.ev_pos[e] + k + (v - vs - n);
+    }
+    kind = 2;
+    return (int64_t)tile_perm((uint64_t)p, C.K);
+}
+
+template <bool kBlocks, int KC>
+__global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : 6)
+    k_async_pi(DevLP L, StepParams P, PiCtx C, int batch) {
+    __shared__ WarpSmem wsm[kPiWarps];
+    __shared__ Deferred wdf[kPiWarps];
+    __shared__ unsigned s_next;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpSmem& sm = wsm[w];
+    Deferred& df = wdf[w];
+    if (threadIdx.x == 0) s_next = 0;
+    if (lane == 0) df.n = 0;
+    __syncthreads();
+    const int64_t V = *C.n_slots;
+    for (int it = 0;; it++) {
+        if (df.n && (it & 3) == 0) run_deferred(L, C, df, sm, lane, false);
+        unsigned k = 0;
+        if (lane == 0) k = atomicAdd(&s_next, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        const int64_t first = ((int64_t)k * gridDim.x + blockIdx.x) * batch;
+        if (first >= V) break;
+        int kind = 2, c = 0;
+        int32_t b = 0;
+        int64_t tile = -1;
+        if (lane < batch && first + lane < V) tile = resolve_slot(C, first + lane, kind, b, c);
+        else kind = 3;  // past the end
+        for (int i = 0; i < batch; i++) {
+            const int ki = __shfl_sync(0xffffffffu, kind, i);
+            if (ki == 3) break;
+            if (ki == 2) {
+                process_tile_pi<kBlocks, KC>(L, P, C, __shfl_sync(0xffffffffu, tile, i), sm, lane, true);
+            } else {
+                const int32_t bi = __shfl_sync(0xffffffffu, b, i);
+                const int ci = __shfl_sync(0xffffffffu, c, i);
+                if (ki == 1) {
+                    job_gather<kBlocks, KC>(L, P, C, bi, ci, sm, lane);
+                } else if (job_ready(C, bi, lane)) {
+                    job_scatter(L, C, bi, ci, sm, lane);
+                } else {  // not ready: keep it (wait only when the list is full)
+                    if (df.n == kDefer) run_deferred(L, C, df, sm, lane, true);
+                    __syncwarp();
+                    if (lane == 0) {
+                        df.b[df.n] = bi;
+                        df.c[df.n] = ci;
+                        df.n++;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    run_deferred(L, C, df, sm, lane, true);
+}
+
+// ---- per-solve and per-epoch preparation of the big tiles' events
+__global__ void k_list_big(DevLP L, int64_t n_struct_tiles, PiJob* jobs, unsigned long long* count,
+                           unsigned long long* chunks) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_struct_tiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int a, b;
+        scalar_lanes(L, t * 32, a, b);
+        if (a >= b) continue;
+        const int64_t j0 = L.n_blocks * L.k + (t * 32 + a - L.n_blocks);
+        const int64_t cb = L.colptr[j0], ce = L.colptr[j0 + (b - a)];
+        if (ce - cb <= kJobMin) continue;
+        const int32_t n = (int32_t)((ce - cb + kJobChunk - 1) / kJobChunk);
+        if (jobs) {
+            const unsigned long long i = atomicAdd(count, 1ull);
+            jobs[i].tile = t;
+            jobs[i].cb = cb;
+            jobs[i].ce = ce;
+            jobs[i].n_chunks = n;
+        } else {
+            atomicAdd(count, 1ull);
+            atomicAdd(chunks, (unsigned long long)n);
+        }
+    }
+}
+// per epoch: the events of big tile b -- gathers at its position, scatters G later --
+// and the reset of its accumulators
+__global__ void k_events(PiJob* jobs, int64_t nb, PermKeys K, int64_t G, uint64_t* keys, int32_t* vals) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        PiJob& J = jobs[b];
+        const uint64_t p = tile_perm_inv((uint64_t)J.tile, K);
+        const uint64_t ps = p + (uint64_t)G < K.n_tiles ? p + (uint64_t)G : K.n_tiles;
+        keys[2 * b] = (p << 1) | 1u;
+        vals[2 * b] = (int32_t)(2 * b + 1);
+        keys[2 * b + 1] = ps << 1;
+        vals[2 * b + 1] = (int32_t)(2 * b);
+        J.gdone = 0;
+        for (int l = 0; l < 32; l++) J.acc[l] = 0.0f;
+    }
+}
+// first slots of the sorted events and the slot count (one CTA)
+__global__ void __launch_bounds__(1024) k_event_slots(const PiJob* jobs, int64_t n_ev, int64_t n_tiles,
+                                                      const uint64_t* keys, const int32_t* vals, int64_t* ev_pos,
+                                                      int64_t* ev_vstart, int64_t* n_slots) {
+    typedef cub::BlockScan<int64_t, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t e0 = 0; e0 < n_ev; e0 += 1024) {
+        const int64_t e = e0 + threadIdx.x;
+        int64_t delta = 0, pos = 0;
+        if (e < n_ev) {
+            const int32_t v = vals[e];
+            pos = (int64_t)(keys[e] >> 1);
+            delta = jobs[v >> 1].n_chunks - (v & 1);  // slots added (a gather replaces its position)
+        }
+        int64_t excl, total;
+        Scan(tmp).ExclusiveSum(delta, excl, total);
+        if (e < n_ev) {
+            ev_pos[e] = pos;
+            ev_vstart[e] = pos + carry + excl;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_slots = n_tiles + carry;
+}
+__global__ void k_vindex(const int64_t* ev_vstart, int64_t n_ev, const int64_t* n_slots, int64_t n_blocks,
+                         int32_t* vindex) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_blocks; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i << kVShift;
+        if (v >= *n_slots) continue;
+        int64_t lo = 0, hi = n_ev;  // first event with vstart > v
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (ev_vstart[mid] <= v) lo = mid + 1;
+            else hi = mid;
+        }
+        vindex[i] = (int32_t)(lo - 1);
+    }
+}
+
+}  // namespace
+
+// window: at most ~n_tiles / depth tiles in flight (bounded staleness)
+#ifndef THETIS_PI_DEPTH
+#define THETIS_PI_DEPTH 1024
+#endif
+
+int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool serial, uint64_t seed,
+                   cudaEvent_t* epoch_marks, int n_marks) {
+    const DevLP& L = lp->d;
+    cudaStream_t s = lp->stream;
+    StepParams P{};
+    P.beta = beta;
+    P.beta_d = (double)beta;
+    P.inv_beta = (float)(1.0 / (double)beta);
+    P.invLmax = (float)(1.0 / ((double)beta * lp->maxnorm2 + 1.0 / (double)beta));  // Eq. 7
+    P.rule = step_rule;
+    const int64_t n_tiles = (L.U + 31) / 32;
+    const int64_t n_struct = L.n_blocks + L.n_scalar;
+    const int64_t n_struct_tiles = (n_struct + 31) / 32;
+    // big tiles (static per LP): count, then list
+    Carver Cv(lp->temp);
+    unsigned long long* cnt = Cv.take<unsigned long long>(2);
+    CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 16, s));
+    if (n_struct_tiles > 0)
+        k_list_big<<<grid_for(n_struct_tiles, 256), 256, 0, s>>>(L, n_struct_tiles, nullptr, cnt, cnt + 1);
+    unsigned long long hc[2] = {0, 0};
+    CUDA_TRY(lp, cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(lp, cudaStreamSynchronize(s));
+    const int64_t nb = (int64_t)hc[0], n_ev = 2 * nb;
+    const int64_t max_slots = n_tiles + 2 * (int64_t)hc[1];
+    const int64_t n_vblocks = (max_slots >> kVShift) + 1;
+    PiJob* jobs = Cv.take<PiJob>(nb);
+    uint64_t* keys = Cv.take<uint64_t>(2 * n_ev);
+    int32_t* vals = Cv.take<int32_t>(2 * n_ev);
+    int64_t* ev_pos = Cv.take<int64_t>(n_ev);
+    int64_t* ev_vstart = Cv.take<int64_t>(n_ev);
+    int32_t* vindex = Cv.take<int32_t>(n_vblocks);
+    int64_t* n_slots = Cv.take<int64_t>(1);
+    int end_bit = 1;
+    while (((int64_t)1 << (end_bit - 1)) <= n_tiles) end_bit++;
+    size_t sort_bytes = 0;
+    if (n_ev) cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys, keys + n_ev, vals, vals + n_ev, n_ev, 0, end_bit);
+    void* sort_tmp = Cv.take<char>((int64_t)sort_bytes);
+    if (Cv.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async big tiles");
+    if (nb) {
+        CUDA_TRY(lp, cudaMemsetAsync(jobs, 0, nb * sizeof(PiJob), s));
+        CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
+        k_list_big<<<grid_for(n_struct_tiles, 256), 256, 0, s>>>(L, n_struct_tiles, jobs, cnt, nullptr);
+    }
+    const bool blocks = L.n_blocks > 0;
+    const int kind = !blocks ? 0 : L.k <= 8 ? 1 : 2;
+    // grid: the device's resident warps, or fewer so that the window stays ~n_tiles / depth
+    int dev = 0, sms = 0, per_sm = 0;
+    CUDA_TRY(lp, cudaGetDevice(&dev));
+    CUDA_TRY(lp, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (kind == 0) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<false, 1>, kPiWarps * 32, 0));
+    else if (kind == 1) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, 8>, kPiWarps * 32, 0));
+    else CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, kMaxK>, kPiWarps * 32, 0));
+    if (per_sm < 1) per_sm = 1;
+    int64_t warps = (int64_t)per_sm * sms * kPiWarps;
+    int batch = kPiBatch;
+    int64_t window = n_tiles / THETIS_PI_DEPTH;  // tiles in flight
+    if (window < 1) window = 1;
+    if (warps * batch > window) {
+        batch = window >= 4 * kPiWarps ? kPiBatch : 1;
+        warps = window / batch;
+        if (warps < 1) warps = 1;
+    }
+    if (serial) {
+        warps = 1;
+        batch = 1;
+    }
+    const int64_t grid = warps >= kPiWarps ? warps / kPiWarps : 1;
+    const int threads = warps >= kPiWarps ? kPiWarps * 32 : (int)warps * 32;
+    // scatters of a big tile follow its gathers by G positions: a quarter of the window
+    // (a scatter drawn before the steps are known waits in its warp's list), one with a
+    // single worker (right after them)
+    const int64_t G = serial ? 1 : grid * (threads / 32) * batch / 4 + 1;
+    PiCtx C{};
+    C.n_tiles = n_tiles;
+    C.n_struct = n_struct;
+    C.jobs = jobs;
+    C.n_ev = n_ev;
+    C.ev_pos = ev_pos;
+    C.ev_vstart = ev_vstart;
+    C.ev_val = vals + n_ev;
+    C.vindex = vindex;
+    C.n_slots = n_slots;
+    for (int e = 0; e < epochs; e++) {
+        NvtxRange nvtx_("async epoch");
+        C.K = make_perm_keys(n_tiles, seed, e);
+        C.stamp = (uint32_t)(e + 1);
+        if (nb) {
+            k_events<<<grid_for(nb, 256), 256, 0, s>>>(jobs, nb, C.K, G, keys, vals);
+            CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, keys, keys + n_ev, vals, vals + n_ev,
+                                                         n_ev, 0, end_bit, s));
+            k_event_slots<<<1, 1024, 0, s>>>(jobs, n_ev, n_tiles, keys + n_ev, vals + n_ev, ev_pos, ev_vstart, n_slots);
+            k_vindex<<<grid_for(n_vblocks, 256), 256, 0, s>>>(ev_vstart, n_ev, n_slots, n_vblocks, vindex);
+        } else if (e == 0) {
+            CUDA_TRY(lp, cudaMemcpyAsync(n_slots, &n_tiles, 8, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(lp, cudaStreamSynchronize(s));  // (pageable source)
+        }
+        if (n_tiles > 0) {
+            if (kind == 0) k_async_pi<false, 1><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            else if (kind == 1) k_async_pi<true, 8><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            else k_async_pi<true, kMaxK><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+        }
+        if (epoch_marks && e < n_marks) CUDA_TRY(lp, cudaEventRecord(epoch_marks[e], s));
+    }
+    return check_cuda(lp, "async epochs");
+}
+
+}  // namespace thetis

@@ -9,209 +9,29 @@
 //
 // Deterministic mode (R-5): one launch per colour class; units of a class share no
 // row, so plain loads / stores on r are race free and the result equals the
-// sequential sweep.  The fp32 operation sequence is fixed (DESIGN.md §Arithmetic
-// contract): sequential sum over the column in CSC order, each op rounded
-// separately (__fadd_rn / __fmul_rn / __fdiv_rn), so it is bit-identical to the
-// fp32 build of the oracle.
+// sequential sweep.  The fp32 operation sequence is fixed (R-7, SURVEY
+// §8(c).4): the column dot is 1024 virtual lanes, lane l summing the column's entries
+// at CSC positions l, l + 1024, ... from +0, combined by halving (off = 512 .. 1);
+// every operation rounded on its own (__fadd_rn / __fmul_rn / __fdiv_rn), so a thread,
+// a warp or a 1024-thread CTA gives the bits of the fp32 build of the oracle.
 //
-// Async mode (R-6): tiles of 32 consecutive units in a per-epoch keyed
-// permutation; one persistent kernel whose warps are independent workers.  A
-// tile is tile-synchronous (all gathers, then all scatters); tiles run
-// concurrently, Hogwild-style: r is read with L2 loads (ld.global.cg; stale
-// values allowed) and written with red.global.add.f32, so no update is lost.
-// A tile's scalar columns are one contiguous CSC range, read coalesced 32 at a
-// time (register accumulation inside a column, shared atomics across column
-// boundaries).  A tile with more than kHeavy nonzeros (power-law hubs) is split
-// into kChunk pieces that any warp may claim: warps help finish pending heavy
-// tiles (FIFO in draw order) before drawing new positions.  The grid bounds the
-// number of workers to ~n_tiles / kAsyncDepth (bounded staleness).
+// THETIS_MODE_ASYNC (Alg. 1's permuted sweep, Hogwild) lives in async_pi.cu.  This file
+// holds the hub-lag throughput variant THETIS_MODE_ASYNC_HUBLAG (R-22), per
+// epoch: (1) the row pass -- one stream over the rows with a hub endpoint: the hub
+// steps pending from the previous epoch enter r, every slack takes its step, and r is
+// accumulated into the hub (and light) columns' D; (2) the hub step -- every hub column
+// steps from its D, the step stays pending; (3) the permuted light tiles -- a persistent
+// Hogwild kernel (stale reads of r with ld.global.cg, red.global.add.f32 writes, no lost
+// update), tile-synchronous within a tile.
 #include <algorithm>
 #include <array>
 
 #include <cub/cub.cuh>
 
-#include "thetis_internal.cuh"
+#include "scd_device.cuh"
 
 namespace thetis {
 namespace {
-
-constexpr int kWarpsPerBlock = 8;
-constexpr int64_t kDetWarpCol = 32;  // det: columns longer than this use the warp path
-constexpr int64_t kDetCtaCol = 8192; // ... and longer than this a 1024-thread CTA (k_det_long)
-
-struct StepParams {
-    float beta;       // caller's beta
-    float inv_beta;   // fl(1 / beta), async kernels only
-    float invLmax;    // (float)(1 / L_max), L_max in fp64 (Eq. 7)
-    double beta_d;    // (double)beta
-    int rule;         // THETIS_STEP_LMAX / THETIS_STEP_LJ
-};
-
-__device__ __forceinline__ float ld_cg(const float* p) {
-    float v;
-    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-// streaming load of CSC indices (read once per pass; do not keep in L1)
-__device__ __forceinline__ int32_t ld_cs_i32(const int32_t* p) {
-    int32_t v;
-    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ void red_add(float* p, float v) {
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-__device__ __forceinline__ float unit_invL(const StepParams& P, double norm2) {
-    if (P.rule == THETIS_STEP_LMAX) return P.invLmax;
-    return (float)(1.0 / (P.beta_d * norm2 + 1.0 / P.beta_d));
-}
-
-// g = c - ua + beta D + (z - zbar)/beta, each operation rounded on its own (the
-// deterministic contract); the async kernels (not bit-exact by nature) multiply
-// by inv_beta = fl(1/beta) instead of dividing
-__device__ __forceinline__ float grad_from(float c, float ua, float D, float z, float zb, float beta) {
-    float g = __fsub_rn(c, ua);
-    g = __fadd_rn(g, __fmul_rn(beta, D));
-    g = __fadd_rn(g, __fdiv_rn(__fsub_rn(z, zb), beta));
-    return g;
-}
-__device__ __forceinline__ float grad_fast(float c, float ua, float D, float z, float zb, float beta, float inv_beta) {
-    float g = __fsub_rn(c, ua);
-    g = __fadd_rn(g, __fmul_rn(beta, D));
-    g = __fadd_rn(g, __fmul_rn(__fsub_rn(z, zb), inv_beta));
-    return g;
-}
-__device__ __forceinline__ float clamp_lohi(float t, float lo, float hi) {
-    float zn = t < lo ? lo : t;
-    return zn > hi ? hi : zn;
-}
-
-template <bool kAsync>
-__device__ __forceinline__ void col_scatter(const DevLP& L, int64_t j, float d) {
-    if (d == 0.0f) return;
-    for (int64_t t = L.colptr[j]; t < L.colptr[j + 1]; t++) {
-        int64_t row;
-        float a;
-        entry(L, t, row, a);
-        float ad = L.val ? __fmul_rn(a, d) : (a < 0.0f ? -d : d);
-        if (kAsync) red_add(L.r + row, ad);
-        else L.r[row] = __fadd_rn(L.r[row], ad);
-    }
-}
-
-__device__ __forceinline__ float zbar_of(const DevLP& L, int64_t j) { return L.zbar ? L.zbar[j] : 0.0f; }
-__device__ __forceinline__ float ua_of(const DevLP& L, int64_t j) { return L.ubar ? L.ua[j] : 0.0f; }
-
-// scalar structural column, one thread (the contract's column dot, thetis_internal.cuh)
-template <bool kAsync>
-__device__ __forceinline__ void update_scalar_seq(const DevLP& L, const StepParams& P, int64_t j) {
-    float D = col_dot_tree_thread(L, j, L.r);
-    float z = L.z[j];
-    float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
-    float invL = unit_invL(P, col_norm2(L, j));
-    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-    float d = __fsub_rn(zn, z);
-    col_scatter<kAsync>(L, j, d);
-    L.z[j] = zn;
-}
-
-// Euclidean projection onto the simplex (sort descending, ties: smaller index first).
-// KC >= k is the compile-time capacity: every loop runs to KC with a guard, so for
-// small blocks the arrays stay in registers; the sorted order comes from ranks
-// (rank_l = #{m : y_m > y_l, or y_m = y_l and m < l}), and the prefix sums add the
-// sorted values one at a time in that order (the same operation sequence as a sort).
-template <int KC>
-__device__ __forceinline__ void project_simplex(const float* y, int k, float* x) {
-    int rk[KC];
-#pragma unroll
-    for (int l = 0; l < KC; l++) {
-        int c = 0;
-#pragma unroll
-        for (int m = 0; m < KC; m++)
-            if (l < k && m < k && (y[m] > y[l] || (y[m] == y[l] && m < l))) c++;
-        rk[l] = c;
-    }
-    float s = 0.0f, s_rho = 0.0f;
-    int rho = 1;
-#pragma unroll
-    for (int i = 1; i <= KC; i++) {
-        if (i > k) break;
-        float u = 0.0f;
-#pragma unroll
-        for (int l = 0; l < KC; l++)
-            if (l < k && rk[l] == i - 1) u = y[l];
-        s = __fadd_rn(s, u);
-        if (i == 1) s_rho = s;
-        if (__fsub_rn(u, __fdiv_rn(__fsub_rn(s, 1.0f), (float)i)) > 0.0f) { rho = i; s_rho = s; }
-    }
-    float tau = __fdiv_rn(__fsub_rn(s_rho, 1.0f), (float)rho);
-#pragma unroll
-    for (int l = 0; l < KC; l++)
-        if (l < k) {
-            float v = __fsub_rn(y[l], tau);
-            x[l] = v > 0.0f ? v : 0.0f;
-        }
-}
-
-// k-block (App. E): gradient step on the k columns, then projection on the simplex
-template <bool kAsync, int KC>
-__device__ __forceinline__ void update_block_seq(const DevLP& L, const StepParams& P, int64_t u) {
-    const int k = L.k;
-    const int64_t f = u * k;
-    float y[KC], x[KC];
-    double mx = 0.0;
-    if (P.rule == THETIS_STEP_LJ)
-        for (int l = 0; l < k; l++) {
-            double q = col_norm2(L, f + l);
-            mx = q > mx ? q : mx;
-        }
-    const float invL = unit_invL(P, mx);
-#pragma unroll
-    for (int l = 0; l < KC; l++)
-        if (l < k) {
-            int64_t j = f + l;
-            float D = col_dot_tree_thread(L, j, L.r);
-            float g = grad_from(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta);
-            y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
-        }
-    project_simplex<KC>(y, k, x);
-#pragma unroll
-    for (int l = 0; l < KC; l++)
-        if (l < k) {
-            int64_t j = f + l;
-            float d = __fsub_rn(x[l], L.z[j]);
-            col_scatter<kAsync>(L, j, d);
-            L.z[j] = x[l];
-        }
-}
-
-// slack of row i (column j): a = sigma_i e_i, cost 0, bounds [0, inf); the new
-// value from the row's residual rv
-template <bool kFast>
-__device__ __forceinline__ float slack_new(const DevLP& L, const StepParams& P, int64_t i, int64_t j, float sig,
-                                           float rv, float z) {
-    float D = __fadd_rn(0.0f, sig < 0.0f ? -rv : rv);
-    float ua = 0.0f;
-    if (L.ubar) ua = __fadd_rn(0.0f, sig < 0.0f ? -L.ubar[i] : L.ubar[i]);
-    float g = kFast ? grad_fast(0.0f, ua, D, z, zbar_of(L, j), P.beta, P.inv_beta)
-                    : grad_from(0.0f, ua, D, z, zbar_of(L, j), P.beta);
-    float t = __fsub_rn(z, __fmul_rn(g, unit_invL(P, 1.0)));
-    return t < 0.0f ? 0.0f : t;
-}
-// one slack step with a plain read-modify-write of r (rows of distinct slacks differ)
-template <bool kFast>
-__device__ __forceinline__ void update_slack(const DevLP& L, const StepParams& P, int64_t q) {
-    const int64_t i = slack_row_of(L, q);
-    const int64_t j = L.n_s + q;
-    const float sig = row_sigma(L, i);
-    const float rv = L.r[i];
-    const float z = L.z[j];
-    const float zn = slack_new<kFast>(L, P, i, j, sig, rv, z);
-    const float d = __fsub_rn(zn, z);
-    if (d != 0.0f) L.r[i] = __fadd_rn(rv, sig < 0.0f ? -d : d);
-    L.z[j] = zn;
-}
 
 // ------------------------------------------------------------ deterministic
 // one colour class: members are structural units; long scalar columns are
@@ -351,203 +171,7 @@ __global__ void __launch_bounds__(256) k_det_slacks(DevLP L, StepParams P) {
         update_slack<false>(L, P, q);
 }
 
-// ------------------------------------------------------------ async
-constexpr int kBatch = 16;         // permuted positions drawn per atomic by a warp (large grids)
 
-// scalar sub-range [a, b) of the tile's lanes (tiles cover the structural units)
-__device__ __forceinline__ void scalar_lanes(const DevLP& L, int64_t u0, int& a, int& b) {
-    const int64_t s0 = L.n_blocks, s1 = L.n_blocks + L.n_scalar;
-    int64_t lo = u0 > s0 ? u0 : s0, hi = u0 + 32 < s1 ? u0 + 32 : s1;
-    if (hi < lo) hi = lo;
-    a = (int)(lo - u0);
-    b = (int)(hi - u0);
-}
-
-// async column dot / scatter with the loads of eight entries in flight together
-__device__ __forceinline__ float col_dot_async(const DevLP& L, int64_t j) {
-    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
-    float D = 0.0f;
-    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
-        uint32_t raw[8];
-        float rv[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) raw[u] = q0 + u < ce ? (uint32_t)L.rowidx[q0 + u] : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; u++) rv[u] = q0 + u < ce ? ld_cg(L.r + (raw[u] & kRowMask)) : 0.0f;
-#pragma unroll
-        for (int u = 0; u < 8; u++)
-            if (q0 + u < ce) D += L.val ? L.val[q0 + u] * rv[u] : ((raw[u] & kSignBit) ? -rv[u] : rv[u]);
-    }
-    return D;
-}
-__device__ __forceinline__ void col_scatter_async(const DevLP& L, int64_t j, float d) {
-    if (d == 0.0f) return;
-    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
-    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
-        uint32_t raw[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) raw[u] = q0 + u < ce ? (uint32_t)L.rowidx[q0 + u] : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; u++)
-            if (q0 + u < ce) {
-                const float ad = L.val ? __fmul_rn(L.val[q0 + u], d) : ((raw[u] & kSignBit) ? -d : d);
-                red_add(L.r + (raw[u] & kRowMask), ad);
-            }
-    }
-}
-
-// new values of a k-block from the current (possibly stale) residual
-template <int KC>
-__device__ __forceinline__ void block_values(const DevLP& L, const StepParams& P, int64_t u, float* x) {
-    const int k = L.k;
-    const int64_t f = u * k;
-    float y[KC];
-    double mx = 0.0;
-    if (P.rule == THETIS_STEP_LJ)
-        for (int l = 0; l < k; l++) {
-            double q = col_norm2(L, f + l);
-            mx = q > mx ? q : mx;
-        }
-    const float invL = unit_invL(P, mx);
-#pragma unroll
-    for (int l = 0; l < KC; l++)
-        if (l < k) {
-            int64_t j = f + l;
-            float D = col_dot_async(L, j);
-            float g = grad_fast(c_int(L, j), ua_of(L, j), D, L.z[j], zbar_of(L, j), P.beta, P.inv_beta);
-            y[l] = __fsub_rn(L.z[j], __fmul_rn(g, invL));
-        }
-    project_simplex<KC>(y, k, x);
-}
-
-// per-warp shared state
-struct WarpSmem {
-    int64_t cp[33];   // column starts of the tile's scalar range (cp[ncols] = end)
-    float acc[32];    // per-column partial dots
-    float d[32];      // per-column steps
-};
-
-struct TileCols {
-    int64_t j0, u0;
-    int a, ncols;
-};
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-// largest column index c with cp[c] <= t (uniform over the warp)
-__device__ __forceinline__ int col_of(const WarpSmem& sm, int ncols, int64_t t) {
-    int lo = 0, hi = ncols - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (sm.cp[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-// partial dots of the tile's columns over the nonzero range [c0, c1), added into
-// sm.acc.  Sub-chunks of 32 lying inside one column accumulate in registers;
-// mixed sub-chunks locate each lane's column and add with shared atomics.
-// (rows below m_defer are left out: the row pass accumulated them into lv)
-__device__ __forceinline__ void gather_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                             int lane, int64_t m_defer) {
-    constexpr int U = 4; // sub-chunks in flight: their loads are issued before any use
-    int c = col_of(sm, ncols, c0);
-    int64_t nb = sm.cp[c + 1];
-    float acc = 0.0f;
-    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
-        uint32_t raw[U];
-        float v[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t t = b0 + 32 * q + lane;
-            raw[q] = t < c1 ? (uint32_t)L.rowidx[t] : 0u;  // re-read by the scatter: keep cached
-        }
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t t = b0 + 32 * q + lane;
-            v[q] = 0.0f;
-            if (t < c1 && (int64_t)(raw[q] & kRowMask) >= m_defer) {
-                const float rv = ld_cg(L.r + (raw[q] & kRowMask));
-                v[q] = L.val ? L.val[t] * rv : ((raw[q] & kSignBit) ? -rv : rv);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t base = b0 + 32 * q;
-            if (base >= c1) break;
-            if (nb <= base) {
-                acc = warp_sum(acc);
-                if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
-                acc = 0.0f;
-                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
-            }
-            const int64_t t = base + lane;
-            if (base + 32 <= nb || c1 <= nb) {
-                acc += v[q];
-            } else if (t < c1 && v[q] != 0.0f) {
-                int col = c;
-                while (sm.cp[col + 1] <= t) col++;
-                atomicAdd(&sm.acc[col], v[q]);
-            }
-        }
-    }
-    acc = warp_sum(acc);
-    if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
-    __syncwarp();
-}
-// r += a_j d_j over the nonzero range [c0, c1), d_j = sm.d[column]; rows below
-// m_defer are left out (the next row pass applies d_j there)
-__device__ __forceinline__ void scatter_range(const DevLP& L, WarpSmem& sm, int ncols, int64_t c0, int64_t c1,
-                                              int lane, int64_t m_defer) {
-    constexpr int U = 4;
-    int c = col_of(sm, ncols, c0);
-    int64_t nb = sm.cp[c + 1];
-    float dc = sm.d[c];
-    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
-        uint32_t raw[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t t = b0 + 32 * q + lane;
-            raw[q] = t < c1 ? (uint32_t)ld_cs_i32(L.rowidx + t) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int64_t base = b0 + 32 * q;
-            if (base >= c1) break;
-            if (nb <= base) {
-                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
-                dc = sm.d[c];
-            }
-            const int64_t t = base + lane;
-            float d = dc;
-            const bool live = t < c1 && (int64_t)(raw[q] & kRowMask) >= m_defer;
-            if (!(base + 32 <= nb || c1 <= nb) && live) {
-                int col = c;
-                while (sm.cp[col + 1] <= t) col++;
-                d = sm.d[col];
-            }
-            if (live && d != 0.0f) {
-                const float a = L.val ? L.val[t] : ((raw[q] & kSignBit) ? -1.0f : 1.0f);
-                red_add(L.r + (raw[q] & kRowMask), L.val ? a * d : (a < 0.0f ? -d : d));
-            }
-        }
-    }
-}
-
-// the coordinate step of lane's column from D = sm.acc[lane]; returns the change
-// (z, c: the column's value and cost, loaded ahead by prefetch_tile)
-__device__ __forceinline__ float scalar_step(const DevLP& L, const StepParams& P, const TileCols& tc, float D,
-                                             int lane, float z, float c) {
-    if (lane >= tc.ncols || (L.unit_fixed && L.unit_fixed[tc.u0 + tc.a + lane])) return 0.0f;
-    const int64_t j = tc.j0 + lane;
-    float g = grad_fast(c, ua_of(L, j), D, z, zbar_of(L, j), P.beta, P.inv_beta);
-    float invL = unit_invL(P, col_norm2(L, j));
-    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-    L.z[j] = zn;
-    return __fsub_rn(zn, z);
-}
 
 // Hub step (R-6): tiles whose scalar columns hold more than kHeavy nonzeros take
 // one synchronous step per epoch.  For VC / MIS (every row = one edge (u, v) with
@@ -642,15 +266,21 @@ __device__ __forceinline__ void add_max_side(const HubCtx& H, int key, float val
         if (lane == 0 && !skip) atomicAdd(key_acc(H, k0), val);
         return;
     }
+    // segmented suffix sums over the contiguous runs only: a key may come back later in
+    // the warp (merged small ranges restart the key sequence), so a lane adds from
+    // lane + o only while lane + o lies before the next run head
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = lane == 0 || prev != key;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned after = lane == 31 ? 0u : heads & (0xFFFFFFFEu << lane);
+    const int seg_end = after ? __ffs(after) - 1 : 32;
     float sv = key != -1 ? val : 0.0f;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const float x = __shfl_down_sync(0xffffffffu, sv, o);
-        const int k2 = __shfl_down_sync(0xffffffffu, key, o);
-        if (lane + o < 32 && k2 == key) sv += x;
+        if (lane + o < seg_end) sv += x;
     }
-    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
-    if (key != -1 && (lane == 0 || prev != key) && !skip) atomicAdd(key_acc(H, key), sv);
+    if (key != -1 && head && !skip) atomicAdd(key_acc(H, key), sv);
 }
 
 // per-row keys of the row pass, built once per solve: .x = the min endpoint's
@@ -994,9 +624,6 @@ __device__ __forceinline__ bool lane_tile(const TilePre& t, int lane, int64_t& c
     if (lane >= t.tc.ncols) ce = cb;
     return __reduce_max_sync(0xffffffffu, (unsigned)(ce - cb)) <= (unsigned)kLaneCol;
 }
-__device__ __forceinline__ float entry_val(const DevLP& L, int64_t t, uint32_t raw) {
-    return L.val ? L.val[t] : ((raw & kSignBit) ? -1.0f : 1.0f);
-}
 __device__ __forceinline__ void process_lane_tile(const DevLP& L, const StepParams& P, const TilePre& t, int lane,
                                                   int64_t cb, int64_t ce) {
     float D = 0.0f;
@@ -1184,36 +811,33 @@ int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out
 // reduced config-4 run leaves the async tolerance; measured)
 constexpr int64_t kAsyncDepth = 32, kAsyncDepthBlocks = 128;
 static int64_t async_workers(int64_t n_tiles, int path) {
-    static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
-    if (!per_sm[path]) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (path == kPathBlocks)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks, kMaxK>, kWarpsPerBlock * 32, 0);
-        else if (path == kPathBlocks8)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathBlocks, 8>, kWarpsPerBlock * 32, 0);
-        else if (path == kPathScalar) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathScalar>, kWarpsPerBlock * 32, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[path], k_async<kPathLight>, kWarpsPerBlock * 32, 0);
-        if (per_sm[path] < 1) per_sm[path] = 1;
-    }
+    // queried per call: occupancy and SM count are per-device properties (a process may
+    // solve on several devices), and the queries are cheap next to a solve
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (path == kPathBlocks)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async<kPathBlocks, kMaxK>, kWarpsPerBlock * 32, 0);
+    else if (path == kPathBlocks8)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async<kPathBlocks, 8>, kWarpsPerBlock * 32, 0);
+    else if (path == kPathScalar) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async<kPathScalar>, kWarpsPerBlock * 32, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async<kPathLight>, kWarpsPerBlock * 32, 0);
+    if (per_sm < 1) per_sm = 1;
     int64_t depth_cap = n_tiles / (path == kPathBlocks || path == kPathBlocks8 ? kAsyncDepthBlocks : kAsyncDepth);
-    int64_t dev_cap = (int64_t)per_sm[path] * sms * kWarpsPerBlock;
+    int64_t dev_cap = (int64_t)per_sm * sms * kWarpsPerBlock;
     int64_t w = depth_cap < dev_cap ? depth_cap : dev_cap;
     return w < 1 ? 1 : w;
 }
 
-// persistent grid of the row pass: one block per SM (shared d / D of one range)
+// persistent grid of the row pass: one block per SM (shared d / D of one range); the
+// dynamic shared-memory attribute is per device, so it is set on every call
 static int64_t pass_blocks() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_rows_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-        cudaFuncSetAttribute(k_rows_pass<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-        cudaFuncSetAttribute(k_rows_pass<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_rows_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+    cudaFuncSetAttribute(k_rows_pass<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+    cudaFuncSetAttribute(k_rows_pass<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
     return sms;
 }
 
@@ -1257,11 +881,45 @@ static int ensure_heavy(thetis_lp* lp) {
     return check_cuda(lp, "heavy tiles");
 }
 
+// Diagnostics: THETIS_EXP switches parts of the hub-lag epoch off to split
+// its cost, so results are wrong by design; only a library built with -DTHETIS_DIAG reads
+// it (tools/diag_rows.py), the production library never does.
+#ifdef THETIS_DIAG
 static int g_exp = getenv("THETIS_EXP") ? atoi(getenv("THETIS_EXP")) : 0;
+#else
+static constexpr int g_exp = 0;
+#endif
 int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                  thetis_solve_stats* st) {
     const DevLP& L = lp->d;
     cudaStream_t s = lp->stream;
+    if (mode == THETIS_MODE_ASYNC || mode == THETIS_MODE_ASYNC_SERIAL) {
+        // the permutation-ordered schedule (async_pi.cu)
+        if (st && lp->ev_epoch.empty()) {
+            lp->ev_epoch.resize(THETIS_MAX_EPOCH_TIMES + 2);
+            for (auto& e : lp->ev_epoch) CUDA_TRY(lp, cudaEventCreate(&e));
+        }
+        if (st) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[0], s));
+        THETIS_TRY(solve_async_pi(lp, beta, step_rule, epochs, mode == THETIS_MODE_ASYNC_SERIAL, seed,
+                                  st ? lp->ev_epoch.data() + 1 : nullptr, st ? THETIS_MAX_EPOCH_TIMES : 0));
+        if (st) {
+            CUDA_TRY(lp, cudaStreamSynchronize(s));
+            memset(st, 0, sizeof(*st));
+            st->epochs = epochs;
+            st->L_max = (double)beta * lp->maxnorm2 + 1.0 / (double)beta;
+            st->mode = mode;
+            st->step_rule = step_rule;
+            const int last = epochs < THETIS_MAX_EPOCH_TIMES ? epochs : THETIS_MAX_EPOCH_TIMES;
+            for (int e = 0; e < last; e++) {
+                float ms = 0;
+                CUDA_TRY(lp, cudaEventElapsedTime(&ms, lp->ev_epoch[e], lp->ev_epoch[e + 1]));
+                st->ms_per_epoch[e] = ms;
+                st->ms_total += ms;
+                st->ms_tiles += ms;
+            }
+        }
+        return THETIS_OK;
+    }
     StepParams P{};
     P.beta = beta;
     P.beta_d = (double)beta;
@@ -1312,7 +970,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         }
     }
     const int64_t n_tiles = struct_tiles(L); // (3) permutes the tiles of structural units
-    const bool serial = mode == THETIS_MODE_ASYNC_SERIAL;
+    const bool serial = mode == THETIS_MODE_ASYNC_HUBLAG_SERIAL;
     AsyncCtx AC{};
     HubCtx H{};
     int64_t blocks = 1, hub_blocks = 1, workers = 1;
@@ -1469,6 +1127,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             det_epoch(lp->side);
             if (cudaStreamEndCapture(lp->side, &g) == cudaSuccess && g) {
                 if (cudaGraphInstantiate(&det_graph, g, 0) != cudaSuccess) det_graph = nullptr;
+                lp->det_graph = det_graph;  // owned by the handle from here (released on every path)
                 cudaGraphDestroy(g);
             }
         }
@@ -1477,6 +1136,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     cudaEvent_t ev_start = timed ? lp->ev_epoch[0] : nullptr;
     if (timed) CUDA_TRY(lp, cudaEventRecord(ev_start, s));
     for (int e = 0; e < epochs; e++) {
+        NvtxRange nvtx_(mode == THETIS_MODE_DETERMINISTIC ? "det epoch" : "hub-lag epoch");
         if (mode == THETIS_MODE_DETERMINISTIC) {
             if (det_graph) CUDA_TRY(lp, cudaGraphLaunch(det_graph, s));
             else det_epoch(s);
@@ -1513,7 +1173,6 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         }
         if (timed && e < THETIS_MAX_EPOCH_TIMES) CUDA_TRY(lp, cudaEventRecord(lp->ev_epoch[e + 1], s));
     }
-    lp->det_graph = det_graph;
     THETIS_TRY(check_cuda(lp, "solve"));
     if (timed) {
         CUDA_TRY(lp, cudaStreamSynchronize(s));

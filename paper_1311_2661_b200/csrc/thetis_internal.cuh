@@ -9,6 +9,8 @@
 
 #include "thetis.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: no-ops unless a profiler is attached
+
 namespace thetis {
 
 constexpr int kTile = 32;          // units per async tile (R-6)
@@ -236,6 +238,24 @@ __device__ __forceinline__ uint64_t tile_perm(uint64_t t, const PermKeys& p) {
     while (y >= p.n_tiles) y = feistel_round4(y, p);
     return y;
 }
+// the inverse rounds: (L, R) <- (R ^ F(L, k_r), L) for r = 3 .. 0
+__device__ __forceinline__ uint64_t feistel_inv4(uint64_t y, const PermKeys& p) {
+    const uint32_t mask = p.h >= 32 ? 0xFFFFFFFFu : ((1u << p.h) - 1u);
+    uint32_t L = (uint32_t)(y >> p.h), R = (uint32_t)(y & mask);
+#pragma unroll
+    for (int r = 3; r >= 0; r--) {
+        uint32_t nl = R ^ (fmix32(L ^ p.k[r]) & mask), nr = L;
+        L = nl;
+        R = nr;
+    }
+    return ((uint64_t)L << p.h) | R;
+}
+// pi_e^{-1}(y): the position of tile y in epoch e (cycle-walking the inverse)
+__device__ __forceinline__ uint64_t tile_perm_inv(uint64_t y, const PermKeys& p) {
+    uint64_t x = feistel_inv4(y, p);
+    while (x >= p.n_tiles) x = feistel_inv4(x, p);
+    return x;
+}
 
 // ---- workspace carving (bump allocator; same code for size query and carve)
 struct Carver {
@@ -249,6 +269,14 @@ struct Carver {
         off += (size_t)(count > 0 ? count : 1) * sizeof(T);
         return p;
     }
+};
+
+// NVTX range over a scope (build, solve, epoch, objective, round; host-side enqueue)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 }  // namespace thetis
@@ -314,6 +342,9 @@ int ensure_colouring(thetis_lp* lp, uint64_t seed);
 // scd.cu
 int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed, int step_rule,
                  thetis_solve_stats* st);
+// async_pi.cu: THETIS_MODE_ASYNC / _SERIAL epochs (epoch_marks[e] recorded after epoch e)
+int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool serial, uint64_t seed,
+                   cudaEvent_t* epoch_marks, int n_marks);
 int launch_tile_perm(int64_t n_tiles, uint64_t seed, int64_t epoch, int64_t* out, cudaStream_t s);
 // reduce.cu
 int objective(thetis_lp* lp, float beta, thetis_objective_t* out);

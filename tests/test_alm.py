@@ -119,7 +119,7 @@ def test_alm_async_matches_reference(th):
     g = th.LP.from_graph(VC, gr.n, gr.src, gr.dst, vertex_w=gr.vertex_w)
     st, _, _ = g.solve_alm(cfg.beta, 2.0, 5, 20, mode=th.THETIS_MODE_ASYNC, seed=cfg.solve_seed, target_eps=-1.0)
     ref = RefLP.graph(VC, gr.n, gr.src, gr.dst, vertex_w=gr.vertex_w)
-    rs = ref.solve_alm(cfg.beta, 2.0, 5, 20, mode=oracle.MODE_TILE_SYNC, seed=cfg.solve_seed, target_eps=-1.0)
+    rs = ref.solve_alm(cfg.beta, 2.0, 5, 20, mode=oracle.MODE_ASYNC, seed=cfg.solve_seed, target_eps=-1.0)
     assert st["lp_obj"][-1] == pytest.approx(rs["lp_obj"][-1], rel=1e-3)
     assert st["eps"][-1] <= rs["eps"][-1] + 1e-3
 
@@ -140,10 +140,12 @@ def test_alm_validation(th):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["async", "hublag"])
 @pytest.mark.parametrize("problem", [VC, MIS])
-def test_alm_async_serial_with_hub_step_matches_replay(th, problem):
-    # anchors through the whole async epoch (row pass with anchors, hub step, light tiles
-    # through lv): the one-tile-in-flight kernel equals the oracle's tile-synchronous replay
+def test_alm_async_serial_matches_replay(th, problem, mode):
+    # anchors through the whole async epoch -- THETIS_MODE_ASYNC (big-tile chunks, slack
+    # tiles) or the hub-lag variant (row pass with anchors, hub step, light tiles through
+    # lv): the one-tile-in-flight kernels equal the oracle's replays of their schedules
     rng = np.random.default_rng(2)
     n = 20000
     src = np.concatenate([rng.integers(0, 64, 60000), rng.integers(0, n, 40000)]).astype(np.int32)
@@ -151,8 +153,10 @@ def test_alm_async_serial_with_hub_step_matches_replay(th, problem):
     w = rng.uniform(1, 10, n).astype(np.float32)
     g = th.LP.from_graph(problem, n, src, dst, vertex_w=w)
     r = RefLP.graph(problem, n, src, dst, vertex_w=w)
-    st, ub, zb = g.solve_alm(10.0, 2.0, 3, 6, mode=th.THETIS_MODE_ASYNC_SERIAL, seed=5, target_eps=-1.0)
-    rs = r.solve_alm(10.0, 2.0, 3, 6, mode=oracle.MODE_TILE_SYNC, seed=5, target_eps=-1.0)
+    gm, rm = ((th.THETIS_MODE_ASYNC_SERIAL, oracle.MODE_PI_TILE_SYNC) if mode == "async" else
+              (th.THETIS_MODE_ASYNC_HUBLAG_SERIAL, oracle.MODE_HUBLAG_REPLAY))
+    st, ub, zb = g.solve_alm(10.0, 2.0, 3, 6, mode=gm, seed=5, target_eps=-1.0)
+    rs = r.solve_alm(10.0, 2.0, 3, 6, mode=rm, seed=5, target_eps=-1.0)
     assert st["beta"] == rs["beta"]
     x, rx = g.get_x().cpu().numpy(), r.x()
     assert np.max(np.abs(x - rx)) <= 1e-4 * max(1.0, np.max(np.abs(rx)))

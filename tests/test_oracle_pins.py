@@ -50,6 +50,10 @@ def regular_graph(name):
         return 4, [(a, b) for a in range(4) for b in range(a + 1, 4)], 3
     if name == "Q3":  # cube, 3-regular
         return 8, [(a, a ^ (1 << t)) for a in range(8) for t in range(3) if a < a ^ (1 << t)], 3
+    if name == "K40":  # 39-regular: every tile of 32 vertices holds > 512 incidences (hub tiles)
+        return 40, [(a, b) for a in range(40) for b in range(a + 1, 40)], 39
+    if name == "Circ":  # circulant C_1024(1..12), 24-regular: all its tiles are hub tiles
+        return 1024, [(a, (a + t) % 1024) for a in range(1024) for t in range(1, 13)], 24
     raise KeyError(name)
 
 
@@ -208,6 +212,88 @@ def test_vc_converges_to_closed_form(name, mode):
     np.testing.assert_allclose(x[n:], 0.0, atol=1e-9)
     if name == "K3":
         assert expect == pytest.approx(0.473815, abs=1e-6)
+
+
+@pytest.mark.parametrize("name", ["K3", "Q3", "K40", "Circ"])
+@pytest.mark.parametrize("mode", [oracle.MODE_PI_TILE_SYNC, oracle.MODE_HUBLAG_REPLAY])
+@pytest.mark.parametrize("problem", [VC, MIS])
+def test_replays_converge_to_closed_form(problem, mode, name):
+    # the two replays of the GPU schedules (mode 4: THETIS_MODE_ASYNC's tile-synchronous
+    # sweep; mode 3: the hub-lag schedule, R-22, with hub tiles on K40 / Circ) are other
+    # ways to minimise the same strongly convex f_beta: both reach Eq. 5's unique minimiser
+    # x(beta), the same closed forms as Alg. 1 (VC beta(d beta - 1)/(2 d beta^2 + 1), MIS
+    # beta(d beta + 1)/(2 d beta^2 + 1)), slacks 0
+    # (beta = 2 on the dense graphs: the same closed form, reached in fewer epochs)
+    n, edges, d = regular_graph(name)
+    beta = 2.0 if d > 3 else 10.0
+    lp = RefLP.graph(problem, n, [u for u, _ in edges], [v for _, v in edges], vertex_w=np.ones(n, np.float32))
+    lp.solve(beta, 5000, mode=mode, seed=13, step_rule=oracle.STEP_LMAX)
+    expect = beta * (d * beta + (1 if problem == MIS else -1)) / (2 * d * beta * beta + 1)
+    np.testing.assert_allclose(lp.x()[:n], expect, atol=1e-7)
+    np.testing.assert_allclose(lp.x()[n:], 0.0, atol=1e-7)
+    assert lp.objective(beta)["drift_inf"] < 1e-10
+
+
+@pytest.mark.parametrize("problem", [VC, MIS, MWC])
+def test_pi_tile_sync_replay_is_monotone(problem):
+    # mode 4 under 1/L_max is a descent method epoch by epoch: a structural tile's columns
+    # step together from one state, and with two structural entries per row the tile's
+    # Hessian block has lambda_max <= 2 beta max_j ||a_j||^2 + 1/beta < 2 L_max (Eq. 7), so
+    # the synchronous step with 1/L_max decreases f_beta; slack tiles and MWC edge-label
+    # tiles touch disjoint rows (a diagonal block); k-blocks step one at a time
+    if problem == MWC:
+        side = 12
+        src = [r * side + c for r in range(side) for c in range(side - 1)] + \
+              [r * side + c for r in range(side - 1) for c in range(side)]
+        dst = [s + 1 for s in src[: side * (side - 1)]] + [s + side for s in src[side * (side - 1):]]
+        ew = np.random.default_rng(2).exponential(1.0, len(src)).astype(np.float32)
+        lp = RefLP.graph(MWC, side * side, src, dst, edge_w=ew, k=3, terminals=[0, 11, 143], t_per_label=1)
+    else:
+        src, dst = small_graph(300, 2400, 5)
+        w = np.random.default_rng(4).uniform(1, 10, 300).astype(np.float32)
+        lp = RefLP.graph(problem, 300, src, dst, vertex_w=w)
+    beta = 10.0
+    f = lp.objective(beta)["f_beta"]
+    for e in range(40):
+        lp.solve(beta, 1, mode=oracle.MODE_PI_TILE_SYNC, seed=100 + e, step_rule=oracle.STEP_LMAX)
+        f2 = lp.objective(beta)["f_beta"]
+        assert f2 <= f + 1e-12 * max(1.0, abs(f))
+        f = f2
+
+
+def test_pi_tile_sync_equals_alg1_when_tiles_are_independent():
+    # with n a multiple of 32 and every edge joining two different tiles, no two units of a
+    # tile share a row: the tile-synchronous sweep (mode 4) and Alg. 1 one unit at a time
+    # (mode 1) perform the same operations on the same values -- bit-identical
+    n = 256
+    rng = np.random.default_rng(8)
+    u = rng.integers(0, n, 3000)
+    v = (u + 32 * rng.integers(1, n // 32, 3000)) % n
+    w = rng.uniform(1, 10, n).astype(np.float32)
+    for problem in (VC, MIS):
+        for rule in (oracle.STEP_LMAX, oracle.STEP_LJ):
+            a = RefLP.graph(problem, n, u.astype(np.int32), v.astype(np.int32), vertex_w=w)
+            b = RefLP.graph(problem, n, u.astype(np.int32), v.astype(np.int32), vertex_w=w)
+            a.solve(10.0, 7, mode=oracle.MODE_ASYNC, seed=21, step_rule=rule)
+            b.solve(10.0, 7, mode=oracle.MODE_PI_TILE_SYNC, seed=21, step_rule=rule)
+            assert np.array_equal(a.x(), b.x()) and np.array_equal(a.r(), b.r())
+
+
+def test_hublag_replay_differs_from_alg1_but_not_at_the_fixed_point():
+    # mode 3 is a different schedule (slacks first, hubs one synchronous lagged step): after
+    # a few epochs on a hub graph it is measurably off Alg. 1's trajectory, after many both
+    # sit at the same x(beta) (the distances DESIGN.md R-22 reports at scale)
+    n, edges, d = regular_graph("K40")
+    src, dst = [e[0] for e in edges], [e[1] for e in edges]
+    w = np.random.default_rng(3).uniform(1, 10, n).astype(np.float32)
+    lag = RefLP.graph(VC, n, src, dst, vertex_w=w)
+    alg1 = RefLP.graph(VC, n, src, dst, vertex_w=w)
+    lag.solve(2.0, 5, mode=oracle.MODE_HUBLAG_REPLAY, seed=4)
+    alg1.solve(2.0, 5, mode=oracle.MODE_ASYNC, seed=4)
+    assert np.abs(lag.x() - alg1.x()).max() > 1e-4
+    lag.solve(2.0, 3000, mode=oracle.MODE_HUBLAG_REPLAY, seed=5)
+    alg1.solve(2.0, 3000, mode=oracle.MODE_ASYNC, seed=5)
+    assert np.abs(lag.x() - alg1.x()).max() < 1e-9
 
 
 @pytest.mark.parametrize("name", ["K2", "K3", "C5", "Q3"])
