@@ -54,7 +54,15 @@ def _load(bits: int):
     path = os.path.join(_HERE, f"libthetis_ref{bits}.so")
     if not os.path.exists(path):
         raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
-    L = ctypes.CDLL(path)
+    L = bind(ctypes.CDLL(path))
+    assert L.ref_real_bytes() == bits // 8
+    _LIBS[bits] = L
+    return L
+
+
+def bind(L):
+    """argument / result types of the oracle's C entry points on a loaded library (also used
+    by tests/experiments, whose library includes the oracle's source)"""
     vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
     L.ref_real_bytes.restype = i32
     L.thetis_ref_build_lp.restype = i32
@@ -103,8 +111,6 @@ def _load(bits: int):
     L.thetis_ref_round_x.argtypes = [vp, vp, i32, ctypes.c_uint64, i32, vp, ctypes.POINTER(RefRound)]
     L.thetis_ref_round.restype = i32
     L.thetis_ref_round.argtypes = [vp, i32, ctypes.c_uint64, i32, vp, ctypes.POINTER(RefRound)]
-    assert L.ref_real_bytes() == bits // 8
-    _LIBS[bits] = L
     return L
 
 

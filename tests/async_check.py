@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """GPU async vs the oracle's Alg. 1 trajectory (MODE_ASYNC) on scaled config recipes.
 
-  python tools/async_check.py CASE[,CASE...] [--modes 1,3] [--rules 0,1]
+  python tests/async_check.py CASE[,CASE...] [--modes 1,3] [--rules 0,1]
 
 CASE = cfgname[:scale-or-size]: vc_rmat_26:20, vc_er_1k, mis_er_1m, vc_chunglu_10m:1000000,
 mwc_grid_2048:256.  Prints per case / mode / rule the relative deviations of f_beta, c^T x and
@@ -13,7 +13,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # (tests/ helper: it runs the oracle)
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
