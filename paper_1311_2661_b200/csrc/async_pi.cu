@@ -392,8 +392,13 @@ __device__ __forceinline__ int64_t resolve_slot(const PiCtx& C, int64_t v, int& 
     return (int64_t)tile_perm((uint64_t)p, C.K);
 }
 
+// resident CTAs per SM of the scalar variant (a register cap of 65536 / (minB * 256)); the
+// block variant keeps its registers (k-block arrays)
+#ifndef THETIS_PI_MINB
+#define THETIS_PI_MINB 6
+#endif
 template <bool kBlocks, int KC>
-__global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : 6)
+__global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
     k_async_pi(DevLP L, StepParams P, PiCtx C, int batch) {
     __shared__ WarpSmem wsm[kPiWarps];
     __shared__ Deferred wdf[kPiWarps];
@@ -590,7 +595,10 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     if (per_sm < 1) per_sm = 1;
     int64_t warps = (int64_t)per_sm * sms * kPiWarps;
     int batch = kPiBatch;
-    int64_t window = n_tiles / THETIS_PI_DEPTH;  // tiles in flight
+    // tiles in flight: n_tiles / depth, a quarter of that under 1/L_j, whose steps are up to
+    // max_j ||a_j||^2 times longer than 1/L_max's (the admissible number of
+    // concurrent updaters depends on the Hessian; measured in DESIGN.md R-6)
+    int64_t window = n_tiles / (step_rule == THETIS_STEP_LJ ? 4 * THETIS_PI_DEPTH : THETIS_PI_DEPTH);
     if (window < 1) window = 1;
     if (warps * batch > window) {
         batch = window >= 4 * kPiWarps ? kPiBatch : 1;
@@ -606,7 +614,10 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     // scatters of a big tile follow its gathers by G positions: a quarter of the window
     // (a scatter drawn before the steps are known waits in its warp's list), one with a
     // single worker (right after them)
-    const int64_t G = serial ? 1 : grid * (threads / 32) * batch / 4 + 1;
+#ifndef THETIS_PI_GDIV
+#define THETIS_PI_GDIV 4
+#endif
+    const int64_t G = serial ? 1 : grid * (threads / 32) * batch / THETIS_PI_GDIV + 1;
     PiCtx C{};
     C.n_tiles = n_tiles;
     C.n_struct = n_struct;

@@ -15,14 +15,16 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-RUNS = [  # (config, mode, epochs cap)
-    ("vc_er_1k", 0, None), ("vc_er_1k", 1, None),
-    ("mis_er_1m", 0, None), ("mis_er_1m", 1, None),
-    ("vc_chunglu_10m", 0, 3), ("vc_chunglu_10m", 1, None),
-    ("mwc_grid_2048", 0, None), ("mwc_grid_2048", 1, None),
-    ("vc_rmat_26", 1, None),
-    ("sc_1m", 0, None), ("sc_1m", 1, None),  # NEXT-3 set cover (not a BASELINE config)
+RUNS = [  # (config, mode, step rule, epochs cap); modes: 0 det, 1 async (Alg. 1 order), 3 hub-lag
+    ("vc_er_1k", 0, 0, None), ("vc_er_1k", 1, 0, None), ("vc_er_1k", 3, 0, None),
+    ("mis_er_1m", 0, 0, None), ("mis_er_1m", 1, 0, None), ("mis_er_1m", 3, 0, None),
+    ("vc_chunglu_10m", 0, 0, 3), ("vc_chunglu_10m", 1, 0, None), ("vc_chunglu_10m", 1, 1, None),
+    ("vc_chunglu_10m", 3, 0, None),
+    ("mwc_grid_2048", 0, 0, None), ("mwc_grid_2048", 1, 0, None), ("mwc_grid_2048", 3, 0, None),
+    ("vc_rmat_26", 1, 0, None), ("vc_rmat_26", 1, 1, None), ("vc_rmat_26", 3, 0, None), ("vc_rmat_26", 3, 1, None),
+    ("sc_1m", 0, 0, None), ("sc_1m", 1, 0, None),  # NEXT-3 set cover (not a BASELINE config)
 ]
+MODE_NAME = {0: "det", 1: "async", 3: "hublag"}
 PROBLEM = {"vc_er_1k": 1, "mis_er_1m": 2, "vc_chunglu_10m": 1, "mwc_grid_2048": 3, "vc_rmat_26": 1, "sc_1m": 0}
 
 
@@ -57,7 +59,7 @@ def main():
     peak = float(peaks["hbm_gbs"])
     dev = torch.device("cuda", 0)
     cache = {}
-    for name, mode, cap in RUNS:
+    for name, mode, rule, cap in RUNS:
         if a.only and a.only not in name:
             continue
         prob = PROBLEM[name]
@@ -93,7 +95,7 @@ def main():
             else:
                 lp = th.LP.from_graph(prob, g.n, g.src, g.dst, vertex_w=g.vertex_w, device=dev)
         epochs = cfg.epochs if cap is None else min(cap, cfg.epochs)
-        st = lp.solve(cfg.beta, epochs, mode=mode, seed=cfg.solve_seed)
+        st = lp.solve(cfg.beta, epochs, mode=mode, seed=cfg.solve_seed, step_rule=rule)
         ms = st["ms_per_epoch"]
         med = statistics.median(ms[1:] if len(ms) > 2 else ms)
         upd = st["coordinate_updates"] / max(st["epochs"], 1)
@@ -121,8 +123,9 @@ def main():
                 e1.record(lp.stream)
                 e1.synchronize()
                 extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
-            extra.update(lp_obj=ob["lp_obj"], eps=ob["max_violation_eps"])
-        out = dict(config=name, mode="det" if mode == 0 else "async", epochs=epochs, ms_epoch_median=med,
+            pass  # (lp_obj and eps are in every line)
+        out = dict(config=name, mode=MODE_NAME[mode], step_rule="LJ" if rule else "LMAX", epochs=epochs,
+                   ms_epoch_median=med, eps=ob["max_violation_eps"], lp_obj=ob["lp_obj"],
                    ms_epoch_first=ms[0], updates_per_s=upd / med * 1e3, nnz_per_s=nnz / med * 1e3,
                    alg_bytes_per_epoch=alg, alg_GBps=alg / med / 1e6, frac_of_measured_hbm=alg / med / 1e6 / peak,
                    colours=st["n_colours"], n_struct=lp.n_struct, m=lp.m, nnz_struct=lp.nnz_struct,
