@@ -117,14 +117,14 @@ static int64_t col_nnz(const ref_lp* lp, int64_t j) {
     return j < lp->n_s ? lp->colptr[j + 1] - lp->colptr[j] : 1;
 }
 /* sequential sum_i a_ij * v_i in ascending row order */
-/* a_j^T v in the deterministic arithmetic contract (R-7; SURVEY §8(c).4,
- * "1024-lane strided, butterfly-combined"): virtual lane l in [0, 1024) sums the
- * column's entries t = l, l + 1024, l + 2048, ... (position in CSC order) from +0,
- * each product rounded before the addition; then the lanes combine by halving,
- * p[l] = p[l] + p[l + off] for l < off, off = 512, 256, ..., 1; the dot is p[0].
- * Lanes at or past the column length hold +0, and x + (+0) = x for every lane
- * value x (no lane ever holds -0: a sum starting from +0 is never -0), so the
- * halving may start at the first off below the column length. */
+/* a_j^T v in the deterministic arithmetic contract (R-7; SURVEY §8(c).4's
+ * "strided, butterfly-combined" dot, with 2^17 virtual lanes since round 2): virtual
+ * lane l in [0, 2^17) sums the column's entries t = l, l + 2^17, l + 2^18, ...
+ * (position in CSC order) from +0, each product rounded before the addition; then the
+ * lanes combine by halving, p[l] = p[l] + p[l + off] for l < off, off = 2^16, ..., 1;
+ * the dot is p[0].  Lanes at or past the column length hold +0, and x + (+0) = x for
+ * every lane value x (no lane ever holds -0: a sum starting from +0 is never -0), so
+ * the halving may start at the first off below the column length. */
 static REAL col_dot(const ref_lp* lp, int64_t j, const REAL* v) {
     if (j >= lp->n_s) {
         int64_t q = j - lp->n_s;
@@ -132,7 +132,7 @@ static REAL col_dot(const ref_lp* lp, int64_t j, const REAL* v) {
         acc = acc + lp->slack_sign[q] * v[lp->slack_row[q]];
         return acc;
     }
-    enum { LANES = 1024 };
+    enum { LANES = 1 << 17 };
     static REAL p[LANES];
     const int64_t len = lp->colptr[j + 1] - lp->colptr[j];
     const int64_t used = len < LANES ? len : LANES;

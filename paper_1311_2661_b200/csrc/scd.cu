@@ -87,26 +87,37 @@ __global__ void __launch_bounds__(256) k_det_mid(DevLP L, StepParams P, const in
     if (lane == 0) L.z[j] = zn;
 }
 
-// det: one 1024-thread CTA per scalar column longer than kDetCtaCol (power-law hubs):
-// thread l is the contract's virtual lane l, the halving goes through shared memory
-// (off >= 32) and warp 0's shuffles; the step on thread 0; then every thread scatters
-__global__ void __launch_bounds__(1024) k_det_long(DevLP L, StepParams P, const int32_t* __restrict__ cols) {
+// det: scalar columns longer than kDetCtaCol (power-law hubs) span many CTAs -- one per
+// 1024 virtual lanes of the contract's 2^17 (R-7): a single CTA runs on a single SM, whose
+// random-access rate capped a hub column (config 3: 110 ms per epoch); in three launches
+// per class:
+//   lanes:   CTA (column, b): thread l' computes lane l = 1024 b + l' (its entries l,
+//            l + 2^17, ... in order) into P[pbase + l];
+//   step:    CTA per column: thread l' combines the lanes l' + 1024 b over b with the
+//            tree's offsets 2^16 .. 1024 (b-halving, bit-reversal stack), then the 1024-lane
+//            halving through shared memory and shuffles; thread 0 takes the step (z, d);
+//   scatter: CTA (column, b): r_i += a_ij d_j over a share of the column's entries
+//            (rows of one class are distinct: plain read-modify-write)
+struct LongBlk { int32_t col, b, nblk; int64_t pbase; };
+__global__ void __launch_bounds__(1024) k_det_long_lanes(DevLP L, const LongBlk* __restrict__ blk, float* __restrict__ Pbuf) {
+    const LongBlk B = blk[blockIdx.x];
+    const int64_t cb = L.colptr[B.col], len = L.colptr[B.col + 1] - cb;
+    const int64_t l = 1024 * (int64_t)B.b + threadIdx.x;
+    Pbuf[B.pbase + l] = l < len ? dot_lane(L, cb, len, l, L.r) : 0.0f;
+}
+__global__ void __launch_bounds__(1024) k_det_long_step(DevLP L, StepParams P, const LongBlk* __restrict__ cols,
+                                                        const float* __restrict__ Pbuf, float* __restrict__ dcol) {
     __shared__ float sp[1024];
-    __shared__ float s_d, s_zn;
-    constexpr int kU = 16;  // loads in flight per thread
+    const LongBlk B = cols[blockIdx.x];
     const int l = threadIdx.x, lane = l & 31;
-    const int64_t j = cols[blockIdx.x];
-    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
-    float p = 0.0f;
-    for (int64_t t0 = cb + l; t0 < ce; t0 += kU * 1024) {
-        float x[kU];
-#pragma unroll
-        for (int q = 0; q < kU; q++) x[q] = t0 + 1024 * q < ce ? dot_term(L, t0 + 1024 * q, L.r) : 0.0f;
-#pragma unroll
-        for (int q = 0; q < kU; q++)
-            if (t0 + 1024 * q < ce) p = __fadd_rn(p, x[q]);
+    int lgb = 0;
+    while ((1 << lgb) < B.nblk) lgb++;
+    TreeStack ts;
+    for (int bb = 0; bb < (1 << lgb); bb++) {
+        const int b = lgb ? (int)(__brev((unsigned)bb) >> (32 - lgb)) : 0;
+        ts.push(b < B.nblk ? Pbuf[B.pbase + 1024 * (int64_t)b + l] : 0.0f);
     }
-    sp[l] = p;
+    sp[l] = ts.st[0];
     __syncthreads();
     for (int off = 512; off >= 32; off >>= 1) {
         if (l < off) sp[l] = __fadd_rn(sp[l], sp[l + off]);
@@ -120,36 +131,33 @@ __global__ void __launch_bounds__(1024) k_det_long(DevLP L, StepParams P, const 
             if (lane < off) q = __fadd_rn(q, o);
         }
         if (l == 0) {
+            const int64_t j = B.col;
             const float z = L.z[j];
             const float g = grad_from(c_int(L, j), ua_of(L, j), q, z, zbar_of(L, j), P.beta);
             const float invL = unit_invL(P, col_norm2(L, j));
             const float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-            s_d = __fsub_rn(zn, z);
-            s_zn = zn;
+            dcol[blockIdx.x] = __fsub_rn(zn, z);
+            L.z[j] = zn;
         }
     }
-    __syncthreads();
-    const float d = s_d;
-    if (d != 0.0f)
-        for (int64_t t0 = cb + l; t0 < ce; t0 += kU * 1024) {
-            int64_t row[kU];
-            float a[kU], rv[kU];
-#pragma unroll
-            for (int q = 0; q < kU; q++) {
-                row[q] = 0;
-                a[q] = 0.0f;
-                if (t0 + 1024 * q < ce) entry(L, t0 + 1024 * q, row[q], a[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < kU; q++) rv[q] = t0 + 1024 * q < ce ? L.r[row[q]] : 0.0f;
-#pragma unroll
-            for (int q = 0; q < kU; q++)
-                if (t0 + 1024 * q < ce) L.r[row[q]] = __fadd_rn(rv[q], L.val ? __fmul_rn(a[q], d) : (a[q] < 0.0f ? -d : d));
-        }
-    if (l == 0) L.z[j] = s_zn;
+}
+__global__ void __launch_bounds__(1024) k_det_long_scatter(DevLP L, const LongBlk* __restrict__ blk,
+                                                           const int32_t* __restrict__ blk_col_idx,
+                                                           const float* __restrict__ dcol) {
+    const LongBlk B = blk[blockIdx.x];
+    const float d = dcol[blk_col_idx[blockIdx.x]];
+    if (d == 0.0f) return;
+    const int64_t cb = L.colptr[B.col], len = L.colptr[B.col + 1] - cb;
+    const int64_t per = (len + B.nblk - 1) / B.nblk, t0 = per * B.b, t1 = t0 + per < len ? t0 + per : len;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += 1024) {
+        int64_t row;
+        float a;
+        entry(L, cb + t, row, a);
+        L.r[row] = __fadd_rn(L.r[row], L.val ? __fmul_rn(a, d) : (a < 0.0f ? -d : d));
+    }
 }
 // the class members' scalar columns longer than kDetWarpCol (unordered): (member
-// position, column, 1 if longer than kDetCtaCol)
+// position, column, 1 if longer than kDetCtaCol, its CTAs of 1024 contract lanes)
 __global__ void k_det_long_list(DevLP L, int64_t S, const int32_t* __restrict__ members, int32_t* pos,
                                 unsigned long long* count) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < S; p += (int64_t)gridDim.x * blockDim.x) {
@@ -159,9 +167,10 @@ __global__ void k_det_long_list(DevLP L, int64_t S, const int32_t* __restrict__ 
         const int64_t len = L.colptr[j + 1] - L.colptr[j];
         if (len > kDetWarpCol) {
             const unsigned long long i = atomicAdd(count, 1ull);
-            pos[3 * i] = (int32_t)p;
-            pos[3 * i + 1] = (int32_t)j;
-            pos[3 * i + 2] = len > kDetCtaCol;
+            pos[4 * i] = (int32_t)p;
+            pos[4 * i + 1] = (int32_t)j;
+            pos[4 * i + 2] = len > kDetCtaCol;
+            pos[4 * i + 3] = (int32_t)((len < kDotLanes ? len : kDotLanes) + 1023) / 1024;  // CTAs of lanes
         }
     }
 }
@@ -929,19 +938,21 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     P.invLmax = (float)(1.0 / Lmax);
     // det: the class members' scalar columns longer than kDetWarpCol, grouped by class
     // (ascending member position): medium ones for k_det_mid, long ones for k_det_long
-    std::vector<int64_t> mid_ptr, long_ptr;
-    int32_t *mid_cols = nullptr, *long_cols = nullptr;
+    std::vector<int64_t> mid_ptr, long_ptr, lblk_ptr;
+    int32_t *mid_cols = nullptr, *lblk_col = nullptr;
+    LongBlk *lblk = nullptr, *lcols = nullptr;
+    float *Pbuf = nullptr, *dcol = nullptr;
     if (mode == THETIS_MODE_DETERMINISTIC) {
         THETIS_TRY(ensure_colouring(lp, seed));
         const int64_t S = L.n_blocks + L.n_scalar;
         mid_ptr.assign(lp->K + 1, 0);
         long_ptr.assign(lp->K + 1, 0);
+        lblk_ptr.assign(lp->K + 1, 0);
         if (S > 0 && L.nnz_s > kDetWarpCol) {
             Carver C(lp->temp);
-            int32_t* pos = C.take<int32_t>(3 * S);
+            int32_t* pos = C.take<int32_t>(4 * S);
             unsigned long long* cnt = C.take<unsigned long long>(1);
             mid_cols = C.take<int32_t>(S);
-            long_cols = C.take<int32_t>(S);
             if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "det long columns");
             CUDA_TRY(lp, cudaMemsetAsync(cnt, 0, 8, s));
             const int64_t n_class = lp->class_ptr[lp->K];
@@ -949,24 +960,55 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             unsigned long long h = 0;
             CUDA_TRY(lp, cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(lp, cudaStreamSynchronize(s));
-            std::vector<std::array<int32_t, 3>> lst(h);
+            std::vector<std::array<int32_t, 4>> lst(h);
             if (h) {
-                CUDA_TRY(lp, cudaMemcpyAsync(lst.data(), pos, h * 12, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(lp, cudaMemcpyAsync(lst.data(), pos, h * 16, cudaMemcpyDeviceToHost, s));
                 CUDA_TRY(lp, cudaStreamSynchronize(s));
             }
             std::sort(lst.begin(), lst.end());
-            std::vector<int32_t> mc, lc;
+            // per class: the mid columns (a warp each), the long columns and their lane CTAs
+            std::vector<int32_t> mc, bci;
+            std::vector<LongBlk> lc, lb;
+            int64_t pmax = 0;
             size_t q = 0;
             for (int64_t c = 0; c < lp->K; c++) {
                 mid_ptr[c] = (int64_t)mc.size();
                 long_ptr[c] = (int64_t)lc.size();
-                for (; q < lst.size() && lst[q][0] < lp->class_ptr[c + 1]; q++) (lst[q][2] ? lc : mc).push_back(lst[q][1]);
+                lblk_ptr[c] = (int64_t)lb.size();
+                int64_t pb = 0;
+                for (; q < lst.size() && lst[q][0] < lp->class_ptr[c + 1]; q++) {
+                    if (!lst[q][2]) {
+                        mc.push_back(lst[q][1]);
+                        continue;
+                    }
+                    const int32_t nblk = lst[q][3];
+                    lc.push_back(LongBlk{lst[q][1], 0, nblk, pb});
+                    for (int32_t b = 0; b < nblk; b++) {
+                        lb.push_back(LongBlk{lst[q][1], b, nblk, pb});
+                        bci.push_back((int32_t)(lc.size() - 1 - long_ptr[c]));
+                    }
+                    pb += 1024 * (int64_t)nblk;
+                }
+                pmax = pb > pmax ? pb : pmax;
             }
             mid_ptr[lp->K] = (int64_t)mc.size();
             long_ptr[lp->K] = (int64_t)lc.size();
+            lblk_ptr[lp->K] = (int64_t)lb.size();
+            lcols = C.take<LongBlk>((int64_t)lc.size());
+            lblk = C.take<LongBlk>((int64_t)lb.size());
+            lblk_col = C.take<int32_t>((int64_t)bci.size());
+            Pbuf = C.take<float>(pmax);
+            int64_t lmax = 0;
+            for (int64_t c = 0; c < lp->K; c++) lmax = std::max(lmax, long_ptr[c + 1] - long_ptr[c]);
+            dcol = C.take<float>(lmax);
+            if (C.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "det long columns");
             if (!mc.empty()) CUDA_TRY(lp, cudaMemcpyAsync(mid_cols, mc.data(), mc.size() * 4, cudaMemcpyHostToDevice, s));
-            if (!lc.empty()) CUDA_TRY(lp, cudaMemcpyAsync(long_cols, lc.data(), lc.size() * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(lp, cudaStreamSynchronize(s));  // `mc`, `lc` are pageable host memory
+            if (!lc.empty()) {
+                CUDA_TRY(lp, cudaMemcpyAsync(lcols, lc.data(), lc.size() * sizeof(LongBlk), cudaMemcpyHostToDevice, s));
+                CUDA_TRY(lp, cudaMemcpyAsync(lblk, lb.data(), lb.size() * sizeof(LongBlk), cudaMemcpyHostToDevice, s));
+                CUDA_TRY(lp, cudaMemcpyAsync(lblk_col, bci.data(), bci.size() * 4, cudaMemcpyHostToDevice, s));
+            }
+            CUDA_TRY(lp, cudaStreamSynchronize(s));  // `mc`, `lc`, `lb`, `bci` are pageable host memory
         }
     }
     const int64_t n_tiles = struct_tiles(L); // (3) permutes the tiles of structural units
@@ -1108,8 +1150,13 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
             if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
             else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
             const int64_t nm = mid_ptr[c + 1] - mid_ptr[c], nl = long_ptr[c + 1] - long_ptr[c];
+            const int64_t nb = lblk_ptr[c + 1] - lblk_ptr[c];
             if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, q>>>(L, P, mid_cols + mid_ptr[c], nm);
-            if (nl > 0) k_det_long<<<(unsigned)nl, 1024, 0, q>>>(L, P, long_cols + long_ptr[c]);
+            if (nl > 0) {
+                k_det_long_lanes<<<(unsigned)nb, 1024, 0, q>>>(L, lblk + lblk_ptr[c], Pbuf);
+                k_det_long_step<<<(unsigned)nl, 1024, 0, q>>>(L, P, lcols + long_ptr[c], Pbuf, dcol);
+                k_det_long_scatter<<<(unsigned)nb, 1024, 0, q>>>(L, lblk + lblk_ptr[c], lblk_col + lblk_ptr[c], dcol);
+            }
         }
         if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, q>>>(L, P);
     };

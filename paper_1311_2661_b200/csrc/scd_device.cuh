@@ -10,7 +10,7 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int64_t kDetWarpCol = 32;  // det: columns longer than this use the warp path
-constexpr int64_t kDetCtaCol = 8192; // ... and longer than this a 1024-thread CTA (k_det_long)
+constexpr int64_t kDetCtaCol = 8192; // ... and longer than this a CTA per 1024 contract lanes (k_det_long_*)
 
 struct StepParams {
     float beta;       // caller's beta

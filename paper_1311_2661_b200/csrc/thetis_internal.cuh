@@ -98,17 +98,26 @@ __device__ __forceinline__ void entry(const DevLP& L, int64_t t, int64_t& row, f
 }
 
 // ---- the column dot a_j^T v of the deterministic arithmetic contract (R-7,
-// SURVEY §8(c).4): virtual lane l in [0, 1024) sums the column's entries at positions
-// t = l, l + 1024, ... (CSC order) from +0, each product rounded on its own; then
-// p[l] += p[l + off] for l < off, off = 512, ..., 1; the dot is p[0].  Lanes past the
-// column hold +0 and adding +0 changes no lane value, so every evaluation below
-// skips them and gives the same bits.
+// SURVEY §8(c).4, widened to kDotLanes lanes in round 2): virtual lane l in [0, 2^17) sums
+// the column's entries at positions t = l, l + 2^17, ... (CSC order) from +0, each product
+// rounded on its own; then p[l] += p[l + off] for l < off, off = 2^16, ..., 1; the dot is
+// p[0].  Lanes past the column hold +0 and adding +0 changes no lane value, so every
+// evaluation below skips them and gives the same bits.  (Columns of <= 2048 entries give
+// the bits of round 1's 1024-lane contract.)
+constexpr int kDotLgLanes = 17;
+constexpr int64_t kDotLanes = (int64_t)1 << kDotLgLanes;
 __device__ __forceinline__ float dot_term(const DevLP& L, int64_t t, const float* v) {
     int64_t row;
     float a;
     entry(L, t, row, a);
     const float x = v[row];
     return L.val ? __fmul_rn(a, x) : (a < 0.0f ? -x : x);
+}
+// the value of virtual lane l: its entries l, l + 2^17, ... summed in order from +0
+__device__ __forceinline__ float dot_lane(const DevLP& L, int64_t cb, int64_t len, int64_t l, const float* v) {
+    float x = 0.0f;
+    for (int64_t t = l; t < len; t += kDotLanes) x = __fadd_rn(x, dot_term(L, cb + t, v));
+    return x;
 }
 // one thread, columns of at most W entries (registers)
 template <int W>
@@ -128,20 +137,11 @@ __device__ __forceinline__ float col_dot_tree16(const DevLP& L, int64_t cb, int6
     if (len <= 16) return col_dot_tree_small<16>(L, cb, len, v);
     return col_dot_tree_small<32>(L, cb, len, v);
 }
-// one thread, any column: the lanes in the order the halving combines them (lane
-// bit-reversal), partial sums on a stack by level
-__device__ __forceinline__ float col_dot_tree_thread(const DevLP& L, int64_t j, const float* v) {
-    const int64_t cb = L.colptr[j], len = L.colptr[j + 1] - cb;
-    if (len <= 32) return col_dot_tree16(L, cb, len, v);
-    int lg = 0;
-    while ((1LL << lg) < len && lg < 10) lg++;
-    const int P = 1 << lg;
-    float st[12];
-    int lv[12], sp = 0;
-    for (int k = 0; k < P; k++) {
-        const int l = (int)(__brev((unsigned)k) >> (32 - lg));
-        float x = 0.0f;
-        for (int64_t t = l; t < len; t += 1024) x = __fadd_rn(x, dot_term(L, cb + t, v));
+// partial sums of a halving tree visited in lane bit-reversal order: a stack by level
+struct TreeStack {
+    float st[20];
+    int lv[20], sp = 0;
+    __device__ __forceinline__ void push(float x) {
         st[sp] = x;
         lv[sp++] = 0;
         while (sp >= 2 && lv[sp - 1] == lv[sp - 2]) {
@@ -150,25 +150,60 @@ __device__ __forceinline__ float col_dot_tree_thread(const DevLP& L, int64_t j, 
             sp--;
         }
     }
-    return st[0];
+};
+// one thread, any column: the lanes in the order the halving combines them (lane
+// bit-reversal), partial sums on a stack by level
+__device__ __forceinline__ float col_dot_tree_thread(const DevLP& L, int64_t j, const float* v) {
+    const int64_t cb = L.colptr[j], len = L.colptr[j + 1] - cb;
+    if (len <= 32) return col_dot_tree16(L, cb, len, v);
+    int lg = 0;
+    while ((1LL << lg) < len && lg < kDotLgLanes) lg++;
+    const int64_t P = (int64_t)1 << lg;
+    TreeStack ts;
+    for (int64_t k = 0; k < P; k++) ts.push(dot_lane(L, cb, len, (int64_t)(__brevll((unsigned long long)k) >> (64 - lg)), v));
+    return ts.st[0];
 }
-// one warp, any column: lane q holds the virtual lanes q + 32 i, i < 32; returns the
-// dot on every lane
+// one warp, any column: lane q holds the virtual lanes l = q + 32 i + 1024 k (i < 32,
+// k < 128): per i the k's combine first (the tree's offsets 2^16 .. 1024), then the i's
+// inside the lane (512 .. 32), then the lanes by shuffles (16 .. 1); returns the dot on
+// every lane
 __device__ __forceinline__ float col_dot_tree_warp(const DevLP& L, int64_t j, const float* v, int lane) {
-    const int64_t cb = L.colptr[j], ce = L.colptr[j + 1];
+    const int64_t cb = L.colptr[j], len = L.colptr[j + 1] - cb;
+    const int64_t span = len < kDotLanes ? len : kDotLanes;
+    const int K = (int)((span + 1023) / 1024);
     float p[32];
-#pragma unroll
-    for (int i = 0; i < 32; i++) p[i] = 0.0f;
-    for (int64_t c0 = cb; c0 < ce; c0 += 1024) {
-        float x[32];
+    if (K <= 1) {  // at most 1024 entries: one per lane slot
 #pragma unroll
         for (int i = 0; i < 32; i++) {
-            const int64_t t = c0 + lane + 32 * i;
-            x[i] = t < ce ? dot_term(L, t, v) : 0.0f;
+            const int64_t t = lane + 32 * i;
+            p[i] = t < len ? __fadd_rn(0.0f, dot_term(L, cb + t, v)) : 0.0f;
         }
+    } else if (K <= 8 && len <= kDotLanes) {  // the k's in registers, a fixed 8-wide halving
+#pragma unroll 4
+        for (int i = 0; i < 32; i++) {
+            float x[8];
 #pragma unroll
-        for (int i = 0; i < 32; i++)
-            if (c0 + lane + 32 * i < ce) p[i] = __fadd_rn(p[i], x[i]);
+            for (int k = 0; k < 8; k++) {
+                const int64_t t = lane + 32 * i + 1024 * k;
+                x[k] = t < len ? __fadd_rn(0.0f, dot_term(L, cb + t, v)) : 0.0f;
+            }
+#pragma unroll
+            for (int s = 4; s >= 1; s >>= 1)
+#pragma unroll
+                for (int k = 0; k < s; k++) x[k] = __fadd_rn(x[k], x[k + s]);
+            p[i] = x[0];
+        }
+    } else {  // long columns (ALM anchors): the k's in bit-reversal order on a stack
+        int lgK = 0;
+        while ((1 << lgK) < K) lgK++;
+        for (int i = 0; i < 32; i++) {
+            TreeStack ts;
+            for (int kk = 0; kk < (1 << lgK); kk++) {
+                const int k = lgK ? (int)(__brev((unsigned)kk) >> (32 - lgK)) : 0;
+                ts.push(dot_lane(L, cb, len, lane + 32 * i + 1024 * (int64_t)k, v));
+            }
+            p[i] = ts.st[0];
+        }
     }
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1)  // off = 512 .. 32: within the lane

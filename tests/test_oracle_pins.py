@@ -701,3 +701,29 @@ def test_column_dot_is_the_contracts_tree():
                        np.zeros(1, np.float32), sense=np.zeros(n, np.int8), bits=32)
     # lane 0 = fl(1e8 + 1) = 1e8; lane 512 = -1e8; off = 512: 1e8 + (-1e8) = 0 -> D = 0
     assert lp.grad(1.0, 0) == 0.0
+
+
+def one_column_lp(rr):
+    n = len(rr)
+    return RefLP.generic(n, 1, np.array([0, n]), np.arange(n, dtype=np.int32), np.ones(n, np.float32),
+                         -np.asarray(rr, np.float32), np.zeros(1, np.float32), sense=np.zeros(n, np.int8), bits=32)
+
+
+def test_column_dot_contract_is_2_to_17_lanes_wide():
+    # R-7 since round 2: 2^17 virtual lanes.  2049 entries, r = 1e8 at 0, 1 at 1024, -1e8 at
+    # 2048: each entry is alone in its lane and the halving pairs lane 0 with lane 2048 first
+    # (off = 2048), then with lane 1024: (1e8 - 1e8) + 1 = 1.  (Round 1's 1024 lanes summed
+    # positions 0, 1024, 2048 in one lane: (1e8 + 1) - 1e8 = 0 in fp32.)
+    rr = np.zeros(2049, np.float32)
+    rr[0], rr[1024], rr[2048] = 1e8, 1.0, -1e8
+    assert one_column_lp(rr).grad(1.0, 0) == 1.0
+    # 2^18 + 1 entries: positions 0, 2^17, 2^18 share lane 0 and add in CSC order,
+    # (1e8 + 1) - 1e8 = 0 -- a 2^19-lane tree would pair 0 with 2^18 first and give 1
+    n = (1 << 18) + 1
+    rr = np.zeros(n, np.float32)
+    rr[0], rr[1 << 17], rr[1 << 18] = 1e8, 1.0, -1e8
+    assert one_column_lp(rr).grad(1.0, 0) == 0.0
+    # the top of the tree: off = 2^16 pairs lane 0 with lane 65536 before lane 1024 joins
+    rr = np.zeros(65537, np.float32)
+    rr[0], rr[65536], rr[1024] = 1e8, -1e8, 1.0
+    assert one_column_lp(rr).grad(1.0, 0) == 1.0

@@ -493,14 +493,17 @@ def test_errors(th):
     assert e.value.code == th.THETIS_ERR_NOT_SUPPORTED
 
 
-@pytest.mark.parametrize("n", [3, 1025, 9000])
+@pytest.mark.parametrize("n", [3, 1025, 2049, 9000, 65537, 140000, 262145])
 def test_det_column_dot_order_cases(th, n):
-    # the contract's lane order decides these sums (see test_column_dot_is_the_contracts_tree):
-    # one column over n EQ rows with large cancelling residuals; thread (3), warp (1025) and
-    # CTA (9000 > 8192) paths must give the oracle's bits
+    # the contract's lane order decides these sums (see test_column_dot_is_the_contracts_tree
+    # and test_column_dot_contract_is_2_to_17_lanes_wide): one column over n EQ rows with large
+    # cancelling residuals; thread (3), warp (1025, 2049) and multi-CTA (9000 .. 2^18 + 1 > 8192:
+    # lanes, step, scatter launches) paths must give the oracle's bits
     rr = np.zeros(n, np.float32)
     rr[0], rr[n // 2], rr[n - 1] = 1e8, -1e8, 1.0
     rr[1:n - 1:7] += 0.25
+    if n > 2048:
+        rr[1024], rr[2048 % n] = 3.0, -1e8
     colptr, rowidx = np.array([0, n]), np.arange(n, dtype=np.int32)
     args = (n, 1, colptr, rowidx, np.ones(n, np.float32))
     g = th.LP.from_csc_csr(*args, np.arange(n + 1, dtype=np.int64), np.zeros(n, np.int32), np.ones(n, np.float32),
