@@ -535,9 +535,15 @@ __global__ void k_vindex(const int64_t* ev_vstart, int64_t n_ev, const int64_t* 
 
 }  // namespace
 
-// window: at most ~n_tiles / depth tiles in flight (bounded staleness)
+// window: at most ~n_tiles / depth tiles in flight (bounded staleness); the
+// depth depends on the step rule: 1/L_j steps are up to max_j ||a_j||^2 times longer than
+// 1/L_max's, and the admissible number of concurrent updaters "depends on ... the diagonal
+// dominance properties of the Hessian"; values measured in DESIGN.md R-6
 #ifndef THETIS_PI_DEPTH
-#define THETIS_PI_DEPTH 1024
+#define THETIS_PI_DEPTH 128
+#endif
+#ifndef THETIS_PI_DEPTH_LJ
+#define THETIS_PI_DEPTH_LJ 4096
 #endif
 
 int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool serial, uint64_t seed,
@@ -595,10 +601,7 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     if (per_sm < 1) per_sm = 1;
     int64_t warps = (int64_t)per_sm * sms * kPiWarps;
     int batch = kPiBatch;
-    // tiles in flight: n_tiles / depth, a quarter of that under 1/L_j, whose steps are up to
-    // max_j ||a_j||^2 times longer than 1/L_max's (the admissible number of
-    // concurrent updaters depends on the Hessian; measured in DESIGN.md R-6)
-    int64_t window = n_tiles / (step_rule == THETIS_STEP_LJ ? 4 * THETIS_PI_DEPTH : THETIS_PI_DEPTH);
+    int64_t window = n_tiles / (step_rule == THETIS_STEP_LJ ? THETIS_PI_DEPTH_LJ : THETIS_PI_DEPTH);
     if (window < 1) window = 1;
     if (warps * batch > window) {
         batch = window >= 4 * kPiWarps ? kPiBatch : 1;

@@ -106,20 +106,20 @@ def main():
         rules = {1: [("VC_HALF", th.THETIS_ROUND_VC_HALF)], 2: [("MIS_GREEDY", th.THETIS_ROUND_MIS_GREEDY),
                                                                  ("MIS_BANSAL", th.THETIS_ROUND_MIS_BANSAL)],
                  3: [("MWC_CKR", th.THETIS_ROUND_MWC_CKR)]}.get(prob, [])
-        for rname, rule in rules:  # device time of one rounding call (CUDA events, 10 repetitions)
+        for rname, rrule in rules:  # device time of one rounding call (CUDA events, 10 repetitions)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            lp.round(rule, seed=3, reps=10)  # warm-up
+            lp.round(rrule, seed=3, reps=10)  # warm-up
             e0.record(lp.stream)
-            _, rr = lp.round(rule, seed=3, reps=10)
+            _, rr = lp.round(rrule, seed=3, reps=10)
             e1.record(lp.stream)
             e1.synchronize()
             extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
         if name == "sc_1m":
-            for rname, rule in (("SC_THRESHOLD", th.THETIS_ROUND_SC_THRESHOLD), ("SC_RANDOM", th.THETIS_ROUND_SC_RANDOM)):
+            for rname, rrule in (("SC_THRESHOLD", th.THETIS_ROUND_SC_THRESHOLD), ("SC_RANDOM", th.THETIS_ROUND_SC_RANDOM)):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                lp.round(rule, seed=3)
+                lp.round(rrule, seed=3)
                 e0.record(lp.stream)
-                _, rr = lp.round(rule, seed=3)
+                _, rr = lp.round(rrule, seed=3)
                 e1.record(lp.stream)
                 e1.synchronize()
                 extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
