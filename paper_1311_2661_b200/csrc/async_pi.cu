@@ -540,7 +540,7 @@ __global__ void k_vindex(const int64_t* ev_vstart, int64_t n_ev, const int64_t* 
 // 1/L_max's, and the admissible number of concurrent updaters "depends on ... the diagonal
 // dominance properties of the Hessian"; values measured in DESIGN.md R-6
 #ifndef THETIS_PI_DEPTH
-#define THETIS_PI_DEPTH 128
+#define THETIS_PI_DEPTH 512
 #endif
 #ifndef THETIS_PI_DEPTH_LJ
 #define THETIS_PI_DEPTH_LJ 4096
