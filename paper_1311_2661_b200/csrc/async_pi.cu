@@ -24,6 +24,17 @@
 // A hub is thus gathered at its position within microseconds by many warps and its
 // step reaches r G positions later: a bounded delay, the async model of P:463-476.
 //
+// Edge-incidence LPs (VC / MIS: every row is x_u + x_v -/+ s_i = 1) run the same order in
+// the *column-sum form* (kGD, R-23): instead of the m residuals the kernel keeps
+// the n column sums D_u = a_u^T r current (fp64, red.global.add.f64).  A vertex tile reads
+// its D_u (coalesced), steps, and adds its step to the D of its neighbours (one RED per
+// nonzero; no gather); a slack tile forms r_i = x_u + x_v -/+ s_i - 1 from x (one coalesced
+// read of its 32 edges, two L2 reads of x) and adds its step to D_u and D_v.  r itself is
+// not touched during the epochs and is recomputed from z on return (r = A z - b, the A2
+// kernel).  Why: Alg. 1's order makes every nonzero a random access; on r (4 B x 1.05e9
+// rows, uniformly accessed) nearly all of them miss the 126 MB L2, on x and D (n values,
+// accessed in proportion to degree) the hot set of a power-law graph is L2-resident.
+//
 // Work distribution: slot batches of kPiBatch; batch b belongs to CTA b mod gridDim,
 // whose warps draw that CTA's batches in order from a shared-memory counter, so all
 // CTAs sweep the slots together without a global atomic per tile, and the slots in
@@ -72,6 +83,8 @@ struct PiCtx {
     const int32_t* vindex;            // per 2^kVShift slots: last event starting at or before, or -1
     const int64_t* n_slots;           // slots this epoch (device)
     uint32_t stamp;                   // epoch stamp of the call (1, 2, ...)
+    const int32_t* nbr;               // kGD: neighbour of CSC entry t
+    double* Dg;                       // kGD: column sums D_u = a_u^T r (fp64, kept current)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -91,6 +104,20 @@ __device__ __forceinline__ int atom_add_release(int32_t* p, int v) {
     int old;
     asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
+}
+
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cg_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int2 ld_cs_int2(const int2* p) {  // streamed once per epoch
+    int2 v;
+    asm volatile("ld.global.cs.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
 }
 
 // the tile's scalar columns: lanes [a, b), first column j0
@@ -121,6 +148,59 @@ __device__ __forceinline__ float slack_lane_gather(const DevLP& L, const StepPar
     L.z[j] = zn;
     const float d = __fsub_rn(zn, z);
     return sig < 0.0f ? -d : d;
+}
+
+// column-sum form (VC / MIS): the slack of row q = (u, v) from x; its step enters D_u and D_v
+__device__ __forceinline__ void slack_lane_gd(const DevLP& L, const StepParams& P, const PiCtx& C, int64_t q) {
+    const int64_t j = L.n_s + q;
+    const float sig = row_sigma(L, q);
+    const int2 e = ld_cs_int2(L.edges + q);
+    const float xu = ld_cg(L.z + e.x), xv = ld_cg(L.z + e.y);
+    const float z = L.z[j];
+    // r_i = -1 + x_u + x_v + sigma s_i, the operation order of A2 (k_recompute_r)
+    float rv = __fadd_rn(__fadd_rn(-1.0f, xu), xv);
+    rv = __fadd_rn(rv, sig < 0.0f ? -z : z);
+    const float zn = slack_new<true>(L, P, q, j, sig, rv, z);
+    if (zn != z) {
+        L.z[j] = zn;
+        const float d = __fsub_rn(zn, z);
+        const double dr = (double)(sig < 0.0f ? -d : d);
+        red_add_f64(C.Dg + e.x, dr);
+        red_add_f64(C.Dg + e.y, dr);
+    }
+}
+// D_v += d_col for the neighbours v of the tile's columns over the nonzero range [c0, c1)
+__device__ __forceinline__ void push_range(const PiCtx& C, WarpSmem& sm, int ncols, int64_t c0, int64_t c1, int lane) {
+    constexpr int U = 4;
+    int c = col_of(sm, ncols, c0);
+    int64_t nb = sm.cp[c + 1];
+    float dc = sm.d[c];
+    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
+        int32_t v[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t t = b0 + 32 * q + lane;
+            v[q] = t < c1 ? ld_cs_i32(C.nbr + t) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t base = b0 + 32 * q;
+            if (base >= c1) break;
+            if (nb <= base) {
+                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+                dc = sm.d[c];
+            }
+            const int64_t t = base + lane;
+            float d = dc;
+            const bool live = t < c1;
+            if (!(base + 32 <= nb || c1 <= nb) && live) {
+                int col = c;
+                while (sm.cp[col + 1] <= t) col++;
+                d = sm.d[col];
+            }
+            if (live && d != 0.0f) red_add_f64(C.Dg + v[q], (double)d);
+        }
+    }
 }
 
 // ---- k-blocks (MWC vertex blocks, App. E): one block at a time in unit order, each by
@@ -202,11 +282,15 @@ __device__ void block_step_warp(const DevLP& L, const StepParams& P, int64_t u, 
 }
 
 // ---- one tile.  scalars = false: the scalar columns are a big tile's (done by chunks)
-template <bool kBlocks, int KC>
+template <bool kBlocks, int KC, bool kGD>
 __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx& C, int64_t tile, WarpSmem& sm,
                                 int lane, bool scalars) {
     const int64_t u = tile * 32 + lane;
     if (tile * 32 >= C.n_struct) {  // slack tile
+        if (kGD) {
+            if (u < L.U) slack_lane_gd(L, P, C, u - C.n_struct);
+            return;
+        }
         float dr = 0.0f;
         int64_t row = 0;
         if (u < L.U) dr = slack_lane_gather(L, P, u - C.n_struct, row);
@@ -248,7 +332,9 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         z = __shfl_sync(0xffffffffu, z, (lane + tc.a) & 31);
         cj = __shfl_sync(0xffffffffu, cj, (lane + tc.a) & 31);
         float D = 0.0f;
-        if (lane_path) {  // one lane per column, eight loads in flight
+        if (kGD) {  // column-sum form: D_j is kept current (lane = column index)
+            if (lane < tc.ncols) D = (float)ld_cg_f64(C.Dg + tc.j0 + lane);
+        } else if (lane_path) {  // one lane per column, eight loads in flight
             for (int64_t q0 = cb; q0 < ce; q0 += 8) {
                 uint32_t raw[8];
                 float rv[8];
@@ -270,11 +356,29 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         const float d = scalar_step(L, P, tc, D, lane, z, cj);  // lane = column index
         sm.d[lane] = d;
         moved = __ballot_sync(0xffffffffu, d != 0.0f);
+        // the column's own sum: D_j += ||a_j||^2 d_j (||a_j||^2 = its nonzero count)
+        if (kGD && d != 0.0f) red_add_f64(C.Dg + tc.j0 + lane, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d);
     }
     __syncwarp();
     // scatters
     if (moved) {
-        if (lane_path) {
+        if (kGD) {
+            if (lane_path) {
+                const int cl = lane - tc.a;
+                const float d = cl >= 0 && cl < 32 ? sm.d[cl] : 0.0f;
+                if (d != 0.0f)
+                    for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+                        int32_t v[8];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) v[q] = q0 + q < ce ? C.nbr[q0 + q] : 0;
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            if (q0 + q < ce) red_add_f64(C.Dg + v[q], (double)d);
+                    }
+            } else {
+                push_range(C, sm, tc.ncols, beg, end, lane);
+            }
+        } else if (lane_path) {
             const int cl = lane - tc.a;
             const float d = cl >= 0 && cl < 32 ? sm.d[cl] : 0.0f;
             if (d != 0.0f)
@@ -289,9 +393,13 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
     }
     __syncwarp();  // the slacks' loads come after the scalars' writes (same-warp ordering)
     if (u >= C.n_struct && u < L.U) {
-        int64_t srow = 0;
-        const float dr = slack_lane_gather(L, P, u - C.n_struct, srow);
-        if (dr != 0.0f) red_add(L.r + srow, dr);
+        if (kGD) {
+            slack_lane_gd(L, P, C, u - C.n_struct);
+        } else {
+            int64_t srow = 0;
+            const float dr = slack_lane_gather(L, P, u - C.n_struct, srow);
+            if (dr != 0.0f) red_add(L.r + srow, dr);
+        }
     }
     __syncwarp();
 }
@@ -299,12 +407,28 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
 // ---- big tiles
 // gather chunk c of big tile b: partial dots of its columns over the chunk; the last
 // one takes the tile's steps (tile-synchronous) and marks them ready
-template <bool kBlocks, int KC>
+template <bool kBlocks, int KC, bool kGD>
 __device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, int32_t b, int c, WarpSmem& sm,
                            int lane) {
     PiJob& J = C.jobs[b];
-    if (c == 0) process_tile_pi<kBlocks, KC>(L, P, C, J.tile, sm, lane, false);  // its other units
+    if (c == 0) process_tile_pi<kBlocks, KC, kGD>(L, P, C, J.tile, sm, lane, false);  // its other units
     const TileCols tc = tile_cols(L, J.tile);
+    if (kGD) {  // column-sum form: nothing to gather; the first chunk's slot takes the tile's steps
+        if (c != 0) return;
+        load_cp(L, tc, sm, lane);
+        float D = 0.0f, z = 0.0f, cj = 0.0f;
+        if (lane < tc.ncols) {
+            D = (float)ld_cg_f64(C.Dg + tc.j0 + lane);
+            z = L.z[tc.j0 + lane];
+            cj = c_int(L, tc.j0 + lane);
+        }
+        const float d = scalar_step(L, P, tc, D, lane, z, cj);
+        J.d[lane] = d;
+        if (d != 0.0f) red_add_f64(C.Dg + tc.j0 + lane, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d);
+        __syncwarp();
+        if (lane == 0) st_release_u32(&J.ready, C.stamp);
+        return;
+    }
     load_cp(L, tc, sm, lane);
     sm.acc[lane] = 0.0f;
     __syncwarp();
@@ -330,6 +454,7 @@ __device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, 
     if (lane == 0) st_release_u32(&J.ready, C.stamp);
 }
 // scatter chunk c of big tile b, whose steps are ready
+template <bool kGD>
 __device__ void job_scatter(const DevLP& L, const PiCtx& C, int32_t b, int c, WarpSmem& sm, int lane) {
     const PiJob& J = C.jobs[b];
     if (lane == 0) (void)ld_acquire_u32(&J.ready);  // the steps and z written before `ready`
@@ -342,7 +467,8 @@ __device__ void job_scatter(const DevLP& L, const PiCtx& C, int32_t b, int c, Wa
     __syncwarp();
     const int64_t c0 = J.cb + (int64_t)c * kJobChunk;
     const int64_t c1 = c0 + kJobChunk < J.ce ? c0 + kJobChunk : J.ce;
-    scatter_range(L, sm, tc.ncols, c0, c1, lane, 0);
+    if (kGD) push_range(C, sm, tc.ncols, c0, c1, lane);
+    else scatter_range(L, sm, tc.ncols, c0, c1, lane, 0);
 }
 __device__ __forceinline__ bool job_ready(const PiCtx& C, int32_t b, int lane) {
     int ok = 0;
@@ -350,11 +476,12 @@ __device__ __forceinline__ bool job_ready(const PiCtx& C, int32_t b, int lane) {
     return __shfl_sync(0xffffffffu, ok, 0);
 }
 // run the deferred scatters that are ready (all of them, waiting, when `drain`)
+template <bool kGD>
 __device__ void run_deferred(const DevLP& L, const PiCtx& C, Deferred& df, WarpSmem& sm, int lane, bool drain) {
     int i = 0;
     while (i < df.n) {
         if (job_ready(C, df.b[i], lane)) {
-            job_scatter(L, C, df.b[i], df.c[i], sm, lane);
+            job_scatter<kGD>(L, C, df.b[i], df.c[i], sm, lane);
             __syncwarp();
             if (lane == 0) {
                 df.b[i] = df.b[df.n - 1];
@@ -397,7 +524,7 @@ __device__ __forceinline__ int64_t resolve_slot(const PiCtx& C, int64_t v, int& 
 #ifndef THETIS_PI_MINB
 #define THETIS_PI_MINB 6
 #endif
-template <bool kBlocks, int KC>
+template <bool kBlocks, int KC, bool kGD>
 __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
     k_async_pi(DevLP L, StepParams P, PiCtx C, int batch) {
     __shared__ WarpSmem wsm[kPiWarps];
@@ -411,7 +538,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
     __syncthreads();
     const int64_t V = *C.n_slots;
     for (int it = 0;; it++) {
-        if (df.n && (it & 3) == 0) run_deferred(L, C, df, sm, lane, false);
+        if (df.n && (it & 3) == 0) run_deferred<kGD>(L, C, df, sm, lane, false);
         unsigned k = 0;
         if (lane == 0) k = atomicAdd(&s_next, 1u);
         k = __shfl_sync(0xffffffffu, k, 0);
@@ -426,16 +553,16 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
             const int ki = __shfl_sync(0xffffffffu, kind, i);
             if (ki == 3) break;
             if (ki == 2) {
-                process_tile_pi<kBlocks, KC>(L, P, C, __shfl_sync(0xffffffffu, tile, i), sm, lane, true);
+                process_tile_pi<kBlocks, KC, kGD>(L, P, C, __shfl_sync(0xffffffffu, tile, i), sm, lane, true);
             } else {
                 const int32_t bi = __shfl_sync(0xffffffffu, b, i);
                 const int ci = __shfl_sync(0xffffffffu, c, i);
                 if (ki == 1) {
-                    job_gather<kBlocks, KC>(L, P, C, bi, ci, sm, lane);
+                    job_gather<kBlocks, KC, kGD>(L, P, C, bi, ci, sm, lane);
                 } else if (job_ready(C, bi, lane)) {
-                    job_scatter(L, C, bi, ci, sm, lane);
+                    job_scatter<kGD>(L, C, bi, ci, sm, lane);
                 } else {  // not ready: keep it (wait only when the list is full)
-                    if (df.n == kDefer) run_deferred(L, C, df, sm, lane, true);
+                    if (df.n == kDefer) run_deferred<kGD>(L, C, df, sm, lane, true);
                     __syncwarp();
                     if (lane == 0) {
                         df.b[df.n] = bi;
@@ -447,7 +574,36 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
             }
         }
     }
-    run_deferred(L, C, df, sm, lane, true);
+    run_deferred<kGD>(L, C, df, sm, lane, true);
+}
+
+// ---- column-sum form: per-LP neighbour lists, per-call column sums
+// nbr[t] = the other endpoint of the row of CSC entry t (column j = vertex j)
+__global__ void k_fill_nbr(DevLP L, int32_t* __restrict__ nbr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = w0 * 32; t0 < L.n_s; t0 += nw * 32) {  // a warp per 32 columns: their CSC range coalesced
+        const int64_t j1 = t0 + 32 < L.n_s ? t0 + 32 : L.n_s;
+        const int64_t cb = L.colptr[t0], ce = L.colptr[j1];
+        int64_t j = t0;
+        int64_t nb = L.colptr[j + 1];
+        for (int64_t t = cb + lane; t < ce; t += 32) {
+            while (nb <= t) nb = L.colptr[++j + 1];
+            const int2 e = L.edges[(uint32_t)L.rowidx[t] & kRowMask];
+            nbr[t] = e.x == (int32_t)j ? e.y : e.x;
+        }
+    }
+}
+// D_u = a_u^T r from the rows (r = A z - b on entry): r_i into both endpoints
+__global__ void k_init_colsum(DevLP L, double* __restrict__ Dg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int2 e = ld_cs_int2(L.edges + i);
+        const double rv = (double)L.r[i];
+        if (rv != 0.0) {
+            red_add_f64(Dg + e.x, rv);
+            red_add_f64(Dg + e.y, rv);
+        }
+    }
 }
 
 // ---- per-solve and per-epoch preparation of the big tiles' events
@@ -590,14 +746,28 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
         k_list_big<<<grid_for(n_struct_tiles, 256), 256, 0, s>>>(L, n_struct_tiles, jobs, cnt, nullptr);
     }
     const bool blocks = L.n_blocks > 0;
-    const int kind = !blocks ? 0 : L.k <= 8 ? 1 : 2;
+    // column-sum form on edge-incidence LPs (R-23); THETIS_ASYNC_RESIDUAL=1 keeps the residual
+    // form there too (same order, same result within rounding: A/B measurements)
+    const char* env_res = getenv("THETIS_ASYNC_RESIDUAL");
+    const bool gd = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr &&
+                    !(env_res && env_res[0] == '1');
+    const int kind = gd ? 3 : !blocks ? 0 : L.k <= 8 ? 1 : 2;
+    if (gd) {
+        if (!lp->nbr_valid) {
+            if (L.n_s > 0) k_fill_nbr<<<grid_for((L.n_s + 31) / 32 * 32, 256), 256, 0, s>>>(L, lp->nbr);
+            lp->nbr_valid = true;
+        }
+        CUDA_TRY(lp, cudaMemsetAsync(lp->Dg, 0, sizeof(double) * (size_t)(L.n_s > 0 ? L.n_s : 1), s));
+        if (L.m > 0) k_init_colsum<<<grid_for(L.m, 256), 256, 0, s>>>(L, lp->Dg);
+    }
     // grid: the device's resident warps, or fewer so that the window stays ~n_tiles / depth
     int dev = 0, sms = 0, per_sm = 0;
     CUDA_TRY(lp, cudaGetDevice(&dev));
     CUDA_TRY(lp, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (kind == 0) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<false, 1>, kPiWarps * 32, 0));
-    else if (kind == 1) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, 8>, kPiWarps * 32, 0));
-    else CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, kMaxK>, kPiWarps * 32, 0));
+    if (kind == 0) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<false, 1, false>, kPiWarps * 32, 0));
+    else if (kind == 1) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, 8, false>, kPiWarps * 32, 0));
+    else if (kind == 2) CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<true, kMaxK, false>, kPiWarps * 32, 0));
+    else CUDA_TRY(lp, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_async_pi<false, 1, true>, kPiWarps * 32, 0));
     if (per_sm < 1) per_sm = 1;
     int64_t warps = (int64_t)per_sm * sms * kPiWarps;
     int batch = kPiBatch;
@@ -631,6 +801,8 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     C.ev_val = vals + n_ev;
     C.vindex = vindex;
     C.n_slots = n_slots;
+    C.nbr = lp->nbr;
+    C.Dg = lp->Dg;
     for (int e = 0; e < epochs; e++) {
         NvtxRange nvtx_("async epoch");
         C.K = make_perm_keys(n_tiles, seed, e);
@@ -646,12 +818,14 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
             CUDA_TRY(lp, cudaStreamSynchronize(s));  // (pageable source)
         }
         if (n_tiles > 0) {
-            if (kind == 0) k_async_pi<false, 1><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
-            else if (kind == 1) k_async_pi<true, 8><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
-            else k_async_pi<true, kMaxK><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            if (kind == 0) k_async_pi<false, 1, false><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            else if (kind == 1) k_async_pi<true, 8, false><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            else if (kind == 2) k_async_pi<true, kMaxK, false><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
+            else k_async_pi<false, 1, true><<<(unsigned)grid, threads, 0, s>>>(L, P, C, batch);
         }
         if (epoch_marks && e < n_marks) CUDA_TRY(lp, cudaEventRecord(epoch_marks[e], s));
     }
+    if (gd) THETIS_TRY(recompute_r(lp));  // r = A z - b on return (the epochs never touched r)
     return check_cuda(lp, "async epochs");
 }
 

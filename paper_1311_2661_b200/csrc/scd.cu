@@ -10,10 +10,11 @@
 // Deterministic mode (R-5): one launch per colour class; units of a class share no
 // row, so plain loads / stores on r are race free and the result equals the
 // sequential sweep.  The fp32 operation sequence is fixed (R-7, SURVEY
-// §8(c).4): the column dot is 1024 virtual lanes, lane l summing the column's entries
-// at CSC positions l, l + 1024, ... from +0, combined by halving (off = 512 .. 1);
+// §8(c).4): the column dot is 2^17 virtual lanes, lane l summing the column's entries
+// at CSC positions l, l + 2^17, ... from +0, combined by halving (off = 2^16 .. 1);
 // every operation rounded on its own (__fadd_rn / __fmul_rn / __fdiv_rn), so a thread,
-// a warp or a 1024-thread CTA gives the bits of the fp32 build of the oracle.
+// a warp, a 1024-thread CTA or a hub column split over many CTAs (1024 lanes each,
+// k_det_long_lanes / _step / _scatter) gives the bits of the fp32 build of the oracle.
 //
 // THETIS_MODE_ASYNC (Alg. 1's permuted sweep, Hogwild) lives in async_pi.cu.  This file
 // holds the hub-lag throughput variant THETIS_MODE_ASYNC_HUBLAG (R-22), per

@@ -337,6 +337,9 @@ struct thetis_lp {
     int32_t* colour = nullptr;     // per structural unit
     int32_t* members = nullptr;    // class members, grouped by class
     int32_t* heavy = nullptr;      // heavy async tiles
+    int32_t* nbr = nullptr;        // VC / MIS: neighbour of CSC entry t (the other endpoint of its row), async_pi.cu
+    double* Dg = nullptr;          // VC / MIS: column sums D_u = a_u^T r kept current during THETIS_MODE_ASYNC
+    bool nbr_valid = false;
     double maxnorm2 = 0;           // max_j ||a_j||^2 over all standard-form columns
     int64_t epoch_updates = 0;     // coordinates updated per epoch (stats)
     int64_t epoch_nnz = 0;         // nonzeros processed per epoch (slack = 1)

@@ -81,3 +81,59 @@ int exp_hubs(ref_lp* lp, float beta, int epochs, uint64_t seed, int rule, int sc
     free(perm); free(hub); free(nv);
     return 0;
 }
+
+/* grouped hub schedule (after a slack-first sweep): structural unit u belongs to group grp[u]
+ * in [0, G) or is light (grp[u] < 0).  Per epoch the groups come in the order of a Fisher-Yates
+ * shuffle from SplitMix64(seed, e) when permute != 0 (else 0..G-1); the units of a group take one
+ * synchronous step from the state left by the earlier groups (Jacobi inside a group, Gauss-Seidel
+ * across groups); then the light tiles in the permuted order, one unit at a time.
+ * jacobi_in_group = 0 makes the units of a group step one at a time too (the sequential order
+ * the grouped schedule approximates). */
+static uint64_t sv_mix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+int exp_groups(ref_lp* lp, float beta, int epochs, uint64_t seed, int rule, const int32_t* grp, int G, int permute,
+               int jacobi_in_group) {
+    step_ctx s = make_ctx(lp, beta, rule);
+    int64_t nsu = lp->n_blocks + lp->n_scalar, nst = (nsu + 31) / 32;
+    int64_t* perm = (int64_t*)xcalloc(nst, sizeof(int64_t));
+    REAL* nv = (REAL*)xcalloc(nsu + 1, sizeof(REAL));
+    /* members of each group, ascending */
+    int64_t* cnt = (int64_t*)xcalloc(G + 1, sizeof(int64_t));
+    for (int64_t u = 0; u < nsu; u++) if (grp[u] >= 0) cnt[grp[u] + 1]++;
+    for (int g = 0; g < G; g++) cnt[g + 1] += cnt[g];
+    int64_t* mem = (int64_t*)xcalloc(cnt[G] + 1, sizeof(int64_t));
+    int64_t* fill = (int64_t*)xcalloc(G + 1, sizeof(int64_t));
+    for (int64_t u = 0; u < nsu; u++) if (grp[u] >= 0) mem[cnt[grp[u]] + fill[grp[u]]++] = u;
+    int* order = (int*)xcalloc(G + 1, sizeof(int));
+    for (int e = 0; e < epochs; e++) {
+        for (int64_t u = nsu; u < lp->U; u++) step_unit(lp, &s, u);
+        for (int g = 0; g < G; g++) order[g] = g;
+        if (permute) {
+            uint64_t st = sv_mix(seed ^ (0xA0761D6478BD642Full * (uint64_t)(e + 1)));
+            for (int g = G - 1; g > 0; g--) {
+                st = sv_mix(st);
+                int j = (int)(st % (uint64_t)(g + 1));
+                int t = order[g]; order[g] = order[j]; order[j] = t;
+            }
+        }
+        for (int q = 0; q < G; q++) {
+            int g = order[q];
+            if (jacobi_in_group) {
+                for (int64_t i = cnt[g]; i < cnt[g + 1]; i++) unit_new_values(lp, &s, mem[i], nv + mem[i]);
+                for (int64_t i = cnt[g]; i < cnt[g + 1]; i++) apply_unit(lp, mem[i], nv + mem[i]);
+            } else {
+                for (int64_t i = cnt[g]; i < cnt[g + 1]; i++) step_unit(lp, &s, mem[i]);
+            }
+        }
+        thetis_ref_tile_perm(nst, seed, e, perm);
+        for (int64_t t = 0; t < nst; t++)
+            for (int64_t u = perm[t] * 32; u < perm[t] * 32 + 32 && u < nsu; u++)
+                if (grp[u] < 0) step_unit(lp, &s, u);
+    }
+    free(perm); free(nv); free(cnt); free(mem); free(fill); free(order);
+    return 0;
+}
