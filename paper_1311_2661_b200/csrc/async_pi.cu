@@ -83,8 +83,13 @@ struct PiCtx {
     const int32_t* vindex;            // per 2^kVShift slots: last event starting at or before, or -1
     const int64_t* n_slots;           // slots this epoch (device)
     uint32_t stamp;                   // epoch stamp of the call (1, 2, ...)
-    const int32_t* nbr;               // kGD: neighbour of CSC entry t
-    double* Dg;                       // kGD: column sums D_u = a_u^T r (fp64, kept current)
+    // kGD (column-sum form): vertices addressed by degree rank
+    const int32_t* rank;              // rank of vertex u
+    const int32_t* nbr;               // rank of the neighbour of CSC entry t
+    const int2* erank;                // ranks of the endpoints of row i
+    float* xr;                        // x by rank (kept current)
+    double* Dg;                       // column sums D_u = a_u^T r by rank (fp64, kept current)
+    int64_t hot;                      // slots below this are kept in L2 (evict_last)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -113,6 +118,61 @@ __device__ __forceinline__ double ld_cg_f64(const double* p) {
     double v;
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
+}
+// L2 eviction policies of the column-sum form: the slots below `hot` (the largest-degree
+// vertices) are kept with evict_last, everything colder passes through with evict_first, so
+// that the ~10^10 bytes streamed per epoch do not turn the hot set over
+struct L2Pol {
+    uint64_t last, first;
+    int64_t hot;
+};
+__device__ __forceinline__ L2Pol make_l2pol(int64_t hot) {
+    L2Pol p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.last));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.first));
+    p.hot = hot;
+    return p;
+}
+__device__ __forceinline__ float ld_x_slot(const float* xr, int slot, const L2Pol& pol) {
+    float v;
+    asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(v) : "l"(xr + slot), "l"(slot < pol.hot ? pol.last : pol.first));
+    return v;
+}
+// D_u lives in HBM / L2 as fp64 (THETIS_GD_DTYPE 0).  Measurement-only alternatives: 1 = fp32
+// (loses small steps against hub sums of ~10^6), 2 = 64-bit fixed point, 2^-32 resolution
+#ifndef THETIS_GD_DTYPE
+#define THETIS_GD_DTYPE 0
+#endif
+__device__ __forceinline__ void red_D_slot(double* Dg, int slot, double v, const L2Pol& pol) {
+    const uint64_t hint = slot < pol.hot ? pol.last : pol.first;
+#if THETIS_GD_DTYPE == 1
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"((float*)Dg + slot), "f"((float)v), "l"(hint) : "memory");
+#elif THETIS_GD_DTYPE == 2
+    asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;"
+                 ::"l"((unsigned long long*)Dg + slot), "l"((unsigned long long)__double2ll_rn(v * 4294967296.0)), "l"(hint) : "memory");
+#else
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(Dg + slot), "d"(v), "l"(hint) : "memory");
+#endif
+}
+__device__ __forceinline__ float ld_D_slot(const double* Dg, int slot) {
+#if THETIS_GD_DTYPE == 1
+    return ld_cg((const float*)Dg + slot);
+#elif THETIS_GD_DTYPE == 2
+    long long q;
+    asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(q) : "l"((const long long*)Dg + slot));
+    return (float)((double)q * (1.0 / 4294967296.0));
+#else
+    return (float)ld_cg_f64(Dg + slot);
+#endif
+}
+__device__ __forceinline__ float ld_cs_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_cs_f32(float* p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 __device__ __forceinline__ int2 ld_cs_int2(const int2* p) {  // streamed once per epoch
     int2 v;
@@ -151,26 +211,28 @@ __device__ __forceinline__ float slack_lane_gather(const DevLP& L, const StepPar
 }
 
 // column-sum form (VC / MIS): the slack of row q = (u, v) from x; its step enters D_u and D_v
-__device__ __forceinline__ void slack_lane_gd(const DevLP& L, const StepParams& P, const PiCtx& C, int64_t q) {
+__device__ __forceinline__ void slack_lane_gd(const DevLP& L, const StepParams& P, const PiCtx& C, const L2Pol& pol,
+                                              int64_t q) {
     const int64_t j = L.n_s + q;
     const float sig = row_sigma(L, q);
-    const int2 e = ld_cs_int2(L.edges + q);
-    const float xu = ld_cg(L.z + e.x), xv = ld_cg(L.z + e.y);
-    const float z = L.z[j];
+    const int2 e = ld_cs_int2(C.erank + q);
+    const float xu = ld_x_slot(C.xr, e.x, pol), xv = ld_x_slot(C.xr, e.y, pol);
+    const float z = ld_cs_f32(L.z + j);
     // r_i = -1 + x_u + x_v + sigma s_i, the operation order of A2 (k_recompute_r)
     float rv = __fadd_rn(__fadd_rn(-1.0f, xu), xv);
     rv = __fadd_rn(rv, sig < 0.0f ? -z : z);
     const float zn = slack_new<true>(L, P, q, j, sig, rv, z);
     if (zn != z) {
-        L.z[j] = zn;
+        st_cs_f32(L.z + j, zn);
         const float d = __fsub_rn(zn, z);
         const double dr = (double)(sig < 0.0f ? -d : d);
-        red_add_f64(C.Dg + e.x, dr);
-        red_add_f64(C.Dg + e.y, dr);
+        red_D_slot(C.Dg, e.x, dr, pol);
+        red_D_slot(C.Dg, e.y, dr, pol);
     }
 }
 // D_v += d_col for the neighbours v of the tile's columns over the nonzero range [c0, c1)
-__device__ __forceinline__ void push_range(const PiCtx& C, WarpSmem& sm, int ncols, int64_t c0, int64_t c1, int lane) {
+__device__ __forceinline__ void push_range(const PiCtx& C, const L2Pol& pol, WarpSmem& sm, int ncols, int64_t c0,
+                                           int64_t c1, int lane) {
     constexpr int U = 4;
     int c = col_of(sm, ncols, c0);
     int64_t nb = sm.cp[c + 1];
@@ -198,7 +260,7 @@ __device__ __forceinline__ void push_range(const PiCtx& C, WarpSmem& sm, int nco
                 while (sm.cp[col + 1] <= t) col++;
                 d = sm.d[col];
             }
-            if (live && d != 0.0f) red_add_f64(C.Dg + v[q], (double)d);
+            if (live && d != 0.0f) red_D_slot(C.Dg, v[q], (double)d, pol);
         }
     }
 }
@@ -283,12 +345,12 @@ __device__ void block_step_warp(const DevLP& L, const StepParams& P, int64_t u, 
 
 // ---- one tile.  scalars = false: the scalar columns are a big tile's (done by chunks)
 template <bool kBlocks, int KC, bool kGD>
-__device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx& C, int64_t tile, WarpSmem& sm,
-                                int lane, bool scalars) {
+__device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx& C, const L2Pol& pol, int64_t tile,
+                                WarpSmem& sm, int lane, bool scalars) {
     const int64_t u = tile * 32 + lane;
     if (tile * 32 >= C.n_struct) {  // slack tile
         if (kGD) {
-            if (u < L.U) slack_lane_gd(L, P, C, u - C.n_struct);
+            if (u < L.U) slack_lane_gd(L, P, C, pol, u - C.n_struct);
             return;
         }
         float dr = 0.0f;
@@ -332,8 +394,12 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         z = __shfl_sync(0xffffffffu, z, (lane + tc.a) & 31);
         cj = __shfl_sync(0xffffffffu, cj, (lane + tc.a) & 31);
         float D = 0.0f;
+        int rk = 0;
         if (kGD) {  // column-sum form: D_j is kept current (lane = column index)
-            if (lane < tc.ncols) D = (float)ld_cg_f64(C.Dg + tc.j0 + lane);
+            if (lane < tc.ncols) {
+                rk = C.rank[tc.j0 + lane];
+                D = ld_D_slot(C.Dg, rk);
+            }
         } else if (lane_path) {  // one lane per column, eight loads in flight
             for (int64_t q0 = cb; q0 < ce; q0 += 8) {
                 uint32_t raw[8];
@@ -356,8 +422,11 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         const float d = scalar_step(L, P, tc, D, lane, z, cj);  // lane = column index
         sm.d[lane] = d;
         moved = __ballot_sync(0xffffffffu, d != 0.0f);
-        // the column's own sum: D_j += ||a_j||^2 d_j (||a_j||^2 = its nonzero count)
-        if (kGD && d != 0.0f) red_add_f64(C.Dg + tc.j0 + lane, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d);
+        // x by rank, and the column's own sum: D_j += ||a_j||^2 d_j (||a_j||^2 = its nonzero count)
+        if (kGD && d != 0.0f) {
+            C.xr[rk] = L.z[tc.j0 + lane];
+            red_D_slot(C.Dg, rk, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d, pol);
+        }
     }
     __syncwarp();
     // scatters
@@ -373,10 +442,10 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
                         for (int q = 0; q < 8; q++) v[q] = q0 + q < ce ? C.nbr[q0 + q] : 0;
 #pragma unroll
                         for (int q = 0; q < 8; q++)
-                            if (q0 + q < ce) red_add_f64(C.Dg + v[q], (double)d);
+                            if (q0 + q < ce) red_D_slot(C.Dg, v[q], (double)d, pol);
                     }
             } else {
-                push_range(C, sm, tc.ncols, beg, end, lane);
+                push_range(C, pol, sm, tc.ncols, beg, end, lane);
             }
         } else if (lane_path) {
             const int cl = lane - tc.a;
@@ -394,7 +463,7 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
     __syncwarp();  // the slacks' loads come after the scalars' writes (same-warp ordering)
     if (u >= C.n_struct && u < L.U) {
         if (kGD) {
-            slack_lane_gd(L, P, C, u - C.n_struct);
+            slack_lane_gd(L, P, C, pol, u - C.n_struct);
         } else {
             int64_t srow = 0;
             const float dr = slack_lane_gather(L, P, u - C.n_struct, srow);
@@ -408,23 +477,28 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
 // gather chunk c of big tile b: partial dots of its columns over the chunk; the last
 // one takes the tile's steps (tile-synchronous) and marks them ready
 template <bool kBlocks, int KC, bool kGD>
-__device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, int32_t b, int c, WarpSmem& sm,
-                           int lane) {
+__device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, const L2Pol& pol, int32_t b, int c,
+                           WarpSmem& sm, int lane) {
     PiJob& J = C.jobs[b];
-    if (c == 0) process_tile_pi<kBlocks, KC, kGD>(L, P, C, J.tile, sm, lane, false);  // its other units
+    if (c == 0) process_tile_pi<kBlocks, KC, kGD>(L, P, C, pol, J.tile, sm, lane, false);  // its other units
     const TileCols tc = tile_cols(L, J.tile);
     if (kGD) {  // column-sum form: nothing to gather; the first chunk's slot takes the tile's steps
         if (c != 0) return;
         load_cp(L, tc, sm, lane);
         float D = 0.0f, z = 0.0f, cj = 0.0f;
+        int rk = 0;
         if (lane < tc.ncols) {
-            D = (float)ld_cg_f64(C.Dg + tc.j0 + lane);
+            rk = C.rank[tc.j0 + lane];
+            D = ld_D_slot(C.Dg, rk);
             z = L.z[tc.j0 + lane];
             cj = c_int(L, tc.j0 + lane);
         }
         const float d = scalar_step(L, P, tc, D, lane, z, cj);
         J.d[lane] = d;
-        if (d != 0.0f) red_add_f64(C.Dg + tc.j0 + lane, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d);
+        if (d != 0.0f) {
+            C.xr[rk] = L.z[tc.j0 + lane];
+            red_D_slot(C.Dg, rk, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d, pol);
+        }
         __syncwarp();
         if (lane == 0) st_release_u32(&J.ready, C.stamp);
         return;
@@ -455,7 +529,7 @@ __device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, 
 }
 // scatter chunk c of big tile b, whose steps are ready
 template <bool kGD>
-__device__ void job_scatter(const DevLP& L, const PiCtx& C, int32_t b, int c, WarpSmem& sm, int lane) {
+__device__ void job_scatter(const DevLP& L, const PiCtx& C, const L2Pol& pol, int32_t b, int c, WarpSmem& sm, int lane) {
     const PiJob& J = C.jobs[b];
     if (lane == 0) (void)ld_acquire_u32(&J.ready);  // the steps and z written before `ready`
     __syncwarp();
@@ -467,7 +541,7 @@ __device__ void job_scatter(const DevLP& L, const PiCtx& C, int32_t b, int c, Wa
     __syncwarp();
     const int64_t c0 = J.cb + (int64_t)c * kJobChunk;
     const int64_t c1 = c0 + kJobChunk < J.ce ? c0 + kJobChunk : J.ce;
-    if (kGD) push_range(C, sm, tc.ncols, c0, c1, lane);
+    if (kGD) push_range(C, pol, sm, tc.ncols, c0, c1, lane);
     else scatter_range(L, sm, tc.ncols, c0, c1, lane, 0);
 }
 __device__ __forceinline__ bool job_ready(const PiCtx& C, int32_t b, int lane) {
@@ -477,11 +551,12 @@ __device__ __forceinline__ bool job_ready(const PiCtx& C, int32_t b, int lane) {
 }
 // run the deferred scatters that are ready (all of them, waiting, when `drain`)
 template <bool kGD>
-__device__ void run_deferred(const DevLP& L, const PiCtx& C, Deferred& df, WarpSmem& sm, int lane, bool drain) {
+__device__ void run_deferred(const DevLP& L, const PiCtx& C, const L2Pol& pol, Deferred& df, WarpSmem& sm, int lane,
+                             bool drain) {
     int i = 0;
     while (i < df.n) {
         if (job_ready(C, df.b[i], lane)) {
-            job_scatter<kGD>(L, C, df.b[i], df.c[i], sm, lane);
+            job_scatter<kGD>(L, C, pol, df.b[i], df.c[i], sm, lane);
             __syncwarp();
             if (lane == 0) {
                 df.b[i] = df.b[df.n - 1];
@@ -524,8 +599,11 @@ __device__ __forceinline__ int64_t resolve_slot(const PiCtx& C, int64_t v, int& 
 #ifndef THETIS_PI_MINB
 #define THETIS_PI_MINB 6
 #endif
+#ifndef THETIS_PI_MINB_GD
+#define THETIS_PI_MINB_GD 6
+#endif
 template <bool kBlocks, int KC, bool kGD>
-__global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
+__global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : kGD ? THETIS_PI_MINB_GD : THETIS_PI_MINB)
     k_async_pi(DevLP L, StepParams P, PiCtx C, int batch) {
     __shared__ WarpSmem wsm[kPiWarps];
     __shared__ Deferred wdf[kPiWarps];
@@ -537,8 +615,9 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
     if (lane == 0) df.n = 0;
     __syncthreads();
     const int64_t V = *C.n_slots;
+    const L2Pol pol = make_l2pol(C.hot);
     for (int it = 0;; it++) {
-        if (df.n && (it & 3) == 0) run_deferred<kGD>(L, C, df, sm, lane, false);
+        if (df.n && (it & 3) == 0) run_deferred<kGD>(L, C, pol, df, sm, lane, false);
         unsigned k = 0;
         if (lane == 0) k = atomicAdd(&s_next, 1u);
         k = __shfl_sync(0xffffffffu, k, 0);
@@ -553,16 +632,16 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
             const int ki = __shfl_sync(0xffffffffu, kind, i);
             if (ki == 3) break;
             if (ki == 2) {
-                process_tile_pi<kBlocks, KC, kGD>(L, P, C, __shfl_sync(0xffffffffu, tile, i), sm, lane, true);
+                process_tile_pi<kBlocks, KC, kGD>(L, P, C, pol, __shfl_sync(0xffffffffu, tile, i), sm, lane, true);
             } else {
                 const int32_t bi = __shfl_sync(0xffffffffu, b, i);
                 const int ci = __shfl_sync(0xffffffffu, c, i);
                 if (ki == 1) {
-                    job_gather<kBlocks, KC, kGD>(L, P, C, bi, ci, sm, lane);
+                    job_gather<kBlocks, KC, kGD>(L, P, C, pol, bi, ci, sm, lane);
                 } else if (job_ready(C, bi, lane)) {
-                    job_scatter<kGD>(L, C, bi, ci, sm, lane);
+                    job_scatter<kGD>(L, C, pol, bi, ci, sm, lane);
                 } else {  // not ready: keep it (wait only when the list is full)
-                    if (df.n == kDefer) run_deferred<kGD>(L, C, df, sm, lane, true);
+                    if (df.n == kDefer) run_deferred<kGD>(L, C, pol, df, sm, lane, true);
                     __syncwarp();
                     if (lane == 0) {
                         df.b[df.n] = bi;
@@ -574,34 +653,67 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : THETIS_PI_MINB)
             }
         }
     }
-    run_deferred<kGD>(L, C, df, sm, lane, true);
+    run_deferred<kGD>(L, C, pol, df, sm, lane, true);
 }
 
-// ---- column-sum form: per-LP neighbour lists, per-call column sums
-// nbr[t] = the other endpoint of the row of CSC entry t (column j = vertex j)
-__global__ void k_fill_nbr(DevLP L, int32_t* __restrict__ nbr) {
+// ---- column-sum form: per-LP ranks and neighbour lists, per-call column sums
+// sort key of vertex u: larger degree first (ties: smaller id, the sort is stable)
+__global__ void k_rank_keys(DevLP L, uint32_t* __restrict__ key, int32_t* __restrict__ id) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < L.n_s; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t deg = L.colptr[u + 1] - L.colptr[u];
+        key[u] = 0xFFFFFFFFu - (uint32_t)(deg < 0xFFFFFFFFLL ? deg : 0xFFFFFFFFLL);
+        id[u] = (int32_t)u;
+    }
+}
+// slot of the vertex at degree rank p.  The hot prefix [0, hot) is transposed in blocks of 32
+// (slot = (p mod hot/32) * 32 + p / (hot/32)): consecutive ranks lie 32 slots (256 B of D) apart, so
+// the REDs into the very largest hubs spread over the L2 slices instead of queueing on one
+__global__ void k_rank_of(int64_t n, int64_t hot, const int32_t* __restrict__ order, int32_t* __restrict__ rank) {
+    const int64_t hb = hot / 32;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        rank[order[p]] = (int32_t)(p < hot ? (p % hb) * 32 + p / hb : p);
+}
+// nbr[t] = rank of the other endpoint of the row of CSC entry t (column j = vertex j); a warp
+// per chunk of kNbrChunk entries, so that hub columns spread over many warps
+constexpr int64_t kNbrChunk = 2048;
+__global__ void k_fill_nbr(DevLP L, const int32_t* __restrict__ rank, int32_t* __restrict__ nbr) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t0 = w0 * 32; t0 < L.n_s; t0 += nw * 32) {  // a warp per 32 columns: their CSC range coalesced
-        const int64_t j1 = t0 + 32 < L.n_s ? t0 + 32 : L.n_s;
-        const int64_t cb = L.colptr[t0], ce = L.colptr[j1];
-        int64_t j = t0;
-        int64_t nb = L.colptr[j + 1];
-        for (int64_t t = cb + lane; t < ce; t += 32) {
+    const int64_t n_chunks = (L.nnz_s + kNbrChunk - 1) / kNbrChunk;
+    for (int64_t c = w0; c < n_chunks; c += nw) {
+        const int64_t c0 = c * kNbrChunk, c1 = c0 + kNbrChunk < L.nnz_s ? c0 + kNbrChunk : L.nnz_s;
+        int64_t lo = 0, hi = L.n_s - 1;  // the column holding entry c0: largest j with colptr[j] <= c0
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (L.colptr[mid] <= c0) lo = mid; else hi = mid - 1;
+        }
+        int64_t j = lo, nb = L.colptr[j + 1];
+        for (int64_t t = c0 + lane; t < c1; t += 32) {
             while (nb <= t) nb = L.colptr[++j + 1];
             const int2 e = L.edges[(uint32_t)L.rowidx[t] & kRowMask];
-            nbr[t] = e.x == (int32_t)j ? e.y : e.x;
+            nbr[t] = rank[e.x == (int32_t)j ? e.y : e.x];
         }
     }
 }
-// D_u = a_u^T r from the rows (r = A z - b on entry): r_i into both endpoints
-__global__ void k_init_colsum(DevLP L, double* __restrict__ Dg) {
+__global__ void k_fill_erank(DevLP L, const int32_t* __restrict__ rank, int2* __restrict__ erank) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
-        const int2 e = ld_cs_int2(L.edges + i);
-        const double rv = (double)L.r[i];
+        const int2 e = L.edges[i];
+        erank[i] = make_int2(rank[e.x], rank[e.y]);
+    }
+}
+// per call: x by rank, and D_u = a_u^T r from the rows (r = A z - b on entry): r_i into both endpoints
+__global__ void k_init_xr(DevLP L, const int32_t* __restrict__ rank, float* __restrict__ xr) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < L.n_s; u += (int64_t)gridDim.x * blockDim.x)
+        xr[rank[u]] = L.z[u];
+}
+__global__ void k_init_colsum(DevLP L, const int2* __restrict__ erank, double* __restrict__ Dg, int64_t hot) {
+    const L2Pol pol = make_l2pol(hot);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int2 e = ld_cs_int2(erank + i);
+        const double rv = (double)ld_cs_f32(L.r + i);
         if (rv != 0.0) {
-            red_add_f64(Dg + e.x, rv);
-            red_add_f64(Dg + e.y, rv);
+            red_D_slot(Dg, e.x, rv, pol);
+            red_D_slot(Dg, e.y, rv, pol);
         }
     }
 }
@@ -715,6 +827,44 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     const int64_t n_tiles = (L.U + 31) / 32;
     const int64_t n_struct = L.n_blocks + L.n_scalar;
     const int64_t n_struct_tiles = (n_struct + 31) / 32;
+    // column-sum form on edge-incidence LPs (R-23); THETIS_ASYNC_RESIDUAL=1 keeps the residual
+    // form there too (same order, same result within rounding: A/B measurements)
+    const char* env_res = getenv("THETIS_ASYNC_RESIDUAL");
+    const bool gd = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr &&
+                    !(env_res && env_res[0] == '1');
+    // hot prefix: the slots kept in L2 with evict_last (12 B each: x and D), a multiple of 32
+#ifndef THETIS_GD_HOT
+#define THETIS_GD_HOT (1 << 22)
+#endif
+    const int64_t hot = (L.n_s < THETIS_GD_HOT ? L.n_s : (int64_t)THETIS_GD_HOT) / 32 * 32;
+#ifdef THETIS_GD_FETCH
+    if (gd) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, THETIS_GD_FETCH);
+#endif
+    // (the setup below uses the scratch region before the big-tile lists are carved from it)
+    if (gd) {
+        if (!lp->nbr_valid) {  // per LP: degree ranks (stable radix sort), neighbour and row ranks
+            NvtxRange nvtx_("async column-sum setup");
+            Carver Tv(lp->temp);
+            uint32_t* rk_key = Tv.take<uint32_t>(2 * L.n_s);
+            int32_t* rk_id = Tv.take<int32_t>(2 * L.n_s);
+            size_t rb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, rb, rk_key, rk_key + L.n_s, rk_id, rk_id + L.n_s, L.n_s, 0, 32);
+            void* rtmp = Tv.take<char>((int64_t)rb);
+            if (Tv.off > lp->temp_bytes) return set_error(lp, THETIS_ERR_WORKSPACE_TOO_SMALL, "async rank sort");
+            if (L.n_s > 0) {
+                k_rank_keys<<<grid_for(L.n_s, 256), 256, 0, s>>>(L, rk_key, rk_id);
+                CUDA_TRY(lp, cub::DeviceRadixSort::SortPairs(rtmp, rb, rk_key, rk_key + L.n_s, rk_id, rk_id + L.n_s,
+                                                             L.n_s, 0, 32, s));
+                k_rank_of<<<grid_for(L.n_s, 256), 256, 0, s>>>(L.n_s, hot, rk_id + L.n_s, lp->rank);
+            }
+            if (L.nnz_s > 0) k_fill_nbr<<<grid_for((L.nnz_s + kNbrChunk - 1) / kNbrChunk * 32, 256), 256, 0, s>>>(L, lp->rank, lp->nbr);
+            if (L.m > 0) k_fill_erank<<<grid_for(L.m, 256), 256, 0, s>>>(L, lp->rank, lp->erank);
+            lp->nbr_valid = true;
+        }
+        CUDA_TRY(lp, cudaMemsetAsync(lp->Dg, 0, sizeof(double) * (size_t)(L.n_s > 0 ? L.n_s : 1), s));
+        if (L.n_s > 0) k_init_xr<<<grid_for(L.n_s, 256), 256, 0, s>>>(L, lp->rank, lp->xr);
+        if (L.m > 0) k_init_colsum<<<grid_for(L.m, 256), 256, 0, s>>>(L, lp->erank, lp->Dg, hot);
+    }
     // big tiles (static per LP): count, then list
     Carver Cv(lp->temp);
     unsigned long long* cnt = Cv.take<unsigned long long>(2);
@@ -746,20 +896,7 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
         k_list_big<<<grid_for(n_struct_tiles, 256), 256, 0, s>>>(L, n_struct_tiles, jobs, cnt, nullptr);
     }
     const bool blocks = L.n_blocks > 0;
-    // column-sum form on edge-incidence LPs (R-23); THETIS_ASYNC_RESIDUAL=1 keeps the residual
-    // form there too (same order, same result within rounding: A/B measurements)
-    const char* env_res = getenv("THETIS_ASYNC_RESIDUAL");
-    const bool gd = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr &&
-                    !(env_res && env_res[0] == '1');
     const int kind = gd ? 3 : !blocks ? 0 : L.k <= 8 ? 1 : 2;
-    if (gd) {
-        if (!lp->nbr_valid) {
-            if (L.n_s > 0) k_fill_nbr<<<grid_for((L.n_s + 31) / 32 * 32, 256), 256, 0, s>>>(L, lp->nbr);
-            lp->nbr_valid = true;
-        }
-        CUDA_TRY(lp, cudaMemsetAsync(lp->Dg, 0, sizeof(double) * (size_t)(L.n_s > 0 ? L.n_s : 1), s));
-        if (L.m > 0) k_init_colsum<<<grid_for(L.m, 256), 256, 0, s>>>(L, lp->Dg);
-    }
     // grid: the device's resident warps, or fewer so that the window stays ~n_tiles / depth
     int dev = 0, sms = 0, per_sm = 0;
     CUDA_TRY(lp, cudaGetDevice(&dev));
@@ -801,8 +938,12 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     C.ev_val = vals + n_ev;
     C.vindex = vindex;
     C.n_slots = n_slots;
+    C.rank = lp->rank;
     C.nbr = lp->nbr;
+    C.erank = lp->erank;
+    C.xr = lp->xr;
     C.Dg = lp->Dg;
+    C.hot = hot;
     for (int e = 0; e < epochs; e++) {
         NvtxRange nvtx_("async epoch");
         C.K = make_perm_keys(n_tiles, seed, e);

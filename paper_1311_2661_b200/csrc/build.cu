@@ -562,7 +562,10 @@ static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* 
     double* red = C.take<double>(kRedBlocks * 16 + 256);
     int32_t* flags = C.take<int32_t>(64);
     // THETIS_MODE_ASYNC on edge-incidence LPs (async_pi.cu): neighbour lists, column sums
+    int32_t* rank = mwc ? nullptr : C.take<int32_t>(n);
     int32_t* nbr = mwc ? nullptr : C.take<int32_t>(nnz);
+    int2* erank = mwc ? nullptr : C.take<int2>(E);
+    float* xr = mwc ? nullptr : C.take<float>(n);
     double* Dg = mwc ? nullptr : C.take<double>(n);
     // temporaries of the build, reused afterwards by colouring and rounding
     size_t temp_start = (C.off + 255) & ~(size_t)255;
@@ -598,7 +601,7 @@ static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* 
         d.colptr = colptr; d.rowidx = rowidx; d.edges = edges; d.c = c; d.z = z; d.r = r; d.ua = ua;
         d.ew = ew; d.term_label = term_label; d.unit_fixed = unit_fixed;
         lp->colour = colour; lp->members = members; lp->heavy = heavy; lp->red = red; lp->flags = flags;
-        lp->nbr = nbr; lp->Dg = Dg; lp->nbr_valid = false;
+        lp->rank = rank; lp->nbr = nbr; lp->erank = erank; lp->xr = xr; lp->Dg = Dg; lp->nbr_valid = false;
         lp->temp = (char*)ws + temp_start;
         lp->temp_bytes = total - temp_start;
         // the by-v sort reuses the key double buffers (2 x 8E bytes); host
@@ -661,7 +664,7 @@ static size_t generic_layout(int64_t m, int64_t n, int64_t nnz, bool has_val, th
         d.rcol = rcol; d.rval = rval; d.b = b; d.sense = sense; d.row_slack = row_slack; d.slack_row = slack_row;
         d.c = c; d.lo = lo; d.hi = hi; d.unit_fixed = unit_fixed; d.z = z; d.r = r; d.ua = ua;
         lp->colour = colour; lp->members = members; lp->heavy = heavy; lp->red = red; lp->flags = flags;
-        lp->nbr = nullptr; lp->Dg = nullptr; lp->nbr_valid = false;
+        lp->rank = nullptr; lp->nbr = nullptr; lp->erank = nullptr; lp->xr = nullptr; lp->Dg = nullptr; lp->nbr_valid = false;
         lp->temp = (char*)ws + temp_start;
         lp->temp_bytes = total - temp_start;
         *scan_buf = scan;

@@ -337,8 +337,13 @@ struct thetis_lp {
     int32_t* colour = nullptr;     // per structural unit
     int32_t* members = nullptr;    // class members, grouped by class
     int32_t* heavy = nullptr;      // heavy async tiles
-    int32_t* nbr = nullptr;        // VC / MIS: neighbour of CSC entry t (the other endpoint of its row), async_pi.cu
-    double* Dg = nullptr;          // VC / MIS: column sums D_u = a_u^T r kept current during THETIS_MODE_ASYNC
+    // VC / MIS, THETIS_MODE_ASYNC in column-sum form (async_pi.cu, R-23); vertices are
+    // addressed by their degree rank (0 = largest degree) so that the hot ones share L2 lines
+    int32_t* rank = nullptr;       // rank of vertex u
+    int32_t* nbr = nullptr;        // rank of the neighbour of CSC entry t (the other endpoint of its row)
+    int2* erank = nullptr;         // ranks of the endpoints of row i
+    float* xr = nullptr;           // x by rank (a copy of z[0, n) kept current during the epochs)
+    double* Dg = nullptr;          // column sums D_u = a_u^T r by rank, kept current during the epochs
     bool nbr_valid = false;
     double maxnorm2 = 0;           // max_j ||a_j||^2 over all standard-form columns
     int64_t epoch_updates = 0;     // coordinates updated per epoch (stats)

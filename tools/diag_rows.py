@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--epochs", type=int, default=6)
     ap.add_argument("--stats", action="store_true")
+    ap.add_argument("--mode", type=int, default=1, help="1 async (Alg. 1 order), 3 hub-lag")
+    ap.add_argument("--rule", type=int, default=0, help="0 1/L_max, 1 1/L_j")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfg = inputs.CONFIGS["vc_rmat_26"]
@@ -84,10 +86,10 @@ def main():
         del u, v, key, k2, eu, ev
         torch.cuda.empty_cache()
     st = th.SolveStats()
-    th._check(th.thetis_solve(h, 10.0, a.epochs, th.THETIS_MODE_ASYNC, cfg.solve_seed, th.THETIS_STEP_LMAX,
+    th._check(th.thetis_solve(h, 10.0, a.epochs, a.mode, cfg.solve_seed, a.rule,
                               ctypes.byref(st)), "solve", h)
     eps = list(st.ms_per_epoch[:a.epochs])
-    out.update(epoch_ms=sorted(eps)[len(eps) // 2], row_pass_ms=st.ms_row_pass / st.row_pass_launches,
+    out.update(epoch_ms=sorted(eps)[len(eps) // 2], row_pass_ms=st.ms_row_pass / max(1, st.row_pass_launches),
                hub_update_ms=st.ms_hub_update / a.epochs, tiles_ms=st.ms_tiles / a.epochs)
     tev[2].record(s)
     ob = th.Objective()
