@@ -133,7 +133,13 @@ __device__ __forceinline__ L2Pol make_l2pol(int64_t hot) {
     p.hot = hot;
     return p;
 }
+// THETIS_GD_EXP (measurement builds only, results wrong by design): 1 drops the REDs into D,
+// 2 drops the slack tiles' reads of x, 4 / 8 drop only the REDs into cold / hot slots
+#ifndef THETIS_GD_EXP
+#define THETIS_GD_EXP 0
+#endif
 __device__ __forceinline__ float ld_x_slot(const float* xr, int slot, const L2Pol& pol) {
+    if (THETIS_GD_EXP & 2) return 0.25f;
     float v;
     asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;"
                  : "=f"(v) : "l"(xr + slot), "l"(slot < pol.hot ? pol.last : pol.first));
@@ -145,6 +151,9 @@ __device__ __forceinline__ float ld_x_slot(const float* xr, int slot, const L2Po
 #define THETIS_GD_DTYPE 0
 #endif
 __device__ __forceinline__ void red_D_slot(double* Dg, int slot, double v, const L2Pol& pol) {
+    if (THETIS_GD_EXP & 1) return;
+    if ((THETIS_GD_EXP & 4) && slot >= pol.hot) return;
+    if ((THETIS_GD_EXP & 8) && slot < pol.hot) return;
     const uint64_t hint = slot < pol.hot ? pol.last : pol.first;
 #if THETIS_GD_DTYPE == 1
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"((float*)Dg + slot), "f"((float)v), "l"(hint) : "memory");
@@ -668,6 +677,8 @@ __global__ void k_rank_keys(DevLP L, uint32_t* __restrict__ key, int32_t* __rest
 // slot of the vertex at degree rank p.  The hot prefix [0, hot) is transposed in blocks of 32
 // (slot = (p mod hot/32) * 32 + p / (hot/32)): consecutive ranks lie 32 slots (256 B of D) apart, so
 // the REDs into the very largest hubs spread over the L2 slices instead of queueing on one
+// (measured on R-MAT 26: 46.8 -> 26.5 ms per epoch).  The colder vertices keep their rank as
+// slot (id order among them measured the same).
 __global__ void k_rank_of(int64_t n, int64_t hot, const int32_t* __restrict__ order, int32_t* __restrict__ rank) {
     const int64_t hb = hot / 32;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)

@@ -590,6 +590,13 @@ static size_t graph_layout(int problem, int64_t n, int64_t E, int k, thetis_lp* 
     t.cub = C.take<char>((int64_t)t.cub_bytes);
     size_t total = C.off;
     size_t post = post_build_temp(S, n_s, n);
+    if (!mwc) {  // THETIS_MODE_ASYNC's per-LP setup (async_pi.cu): the degree sort over n (keys, ids, CUB)
+        size_t sb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, sb, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                        (int32_t*)nullptr, n, 0, 32);
+        const size_t gdt = 16 * (size_t)n + sb + 8 * 256;
+        if (gdt > post) post = gdt;
+    }
     if (!mwc) {  // the async solve's row pass (scd.cu): row keys, hub slots, light slots, items
         const size_t asy = 8 * (size_t)E + 16 * ((size_t)n + 32) + 4 * (size_t)((n + 31) / 32) +
                            16 * (size_t)(2 * (E >> 19) + 2 * ((n >> 14) + 1) + 4) + (size_t)(n >> 14) + (1 << 20);
