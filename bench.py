@@ -331,8 +331,8 @@ def run_thetis(args):
         "data": "synthetic (R-MAT generated on device from seed; BASELINE configs[4])",
         "config": {"workload": f"{CFG_NAME}: VC LP of R-MAT scale {p['scale']} ({E} edge samples, a,b,c = "
                                f"{p['a']},{p['b']},{p['c']}), weights U[1,10), beta {BETA}, {EPOCHS} async "
-                               "epochs (THETIS_MODE_ASYNC: Alg. 1's permuted sweep, Hogwild; STEP_LMAX), VC_HALF "
-                               "rounding",
+                               "epochs (THETIS_MODE_ASYNC: Alg. 1's permuted sweep, Hogwild, column-sum form "
+                               "R-23; STEP_LMAX), VC_HALF rounding",
                    "step": "build + 20 SCD epochs + reductions + rounding",
                    "vertices": n, "unique_edges_rows": int(dims.m), "coordinates": int(dims.N),
                    "nnz_struct": int(dims.nnz_struct), "l2": "inputs (8.6 GB edge list) and state exceed the L2",
@@ -345,8 +345,9 @@ def run_thetis(args):
                      "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of "
                                        "one k_async_pi launch (ncu --set full on this command), not measured in "
                                        "this run",
-                     "kernel": "k_async_pi: one SCD epoch of THETIS_MODE_ASYNC (one launch per epoch; CUDA events "
-                               "around each epoch on the launching stream; SURVEY 8(d) bytes per epoch)",
+                     "kernel": "k_async_pi<kGD>: one SCD epoch of THETIS_MODE_ASYNC in column-sum form (one launch per "
+                               "epoch; CUDA events around each epoch on the launching stream; SURVEY 8(d) bytes "
+                               "per epoch)",
                      "peak_source": peak_src},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),

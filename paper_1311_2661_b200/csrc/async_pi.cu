@@ -838,11 +838,15 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     const int64_t n_tiles = (L.U + 31) / 32;
     const int64_t n_struct = L.n_blocks + L.n_scalar;
     const int64_t n_struct_tiles = (n_struct + 31) / 32;
-    // column-sum form on edge-incidence LPs (R-23); THETIS_ASYNC_RESIDUAL=1 keeps the residual
-    // form there too (same order, same result within rounding: A/B measurements)
-    const char* env_res = getenv("THETIS_ASYNC_RESIDUAL");
-    const bool gd = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr &&
-                    !(env_res && env_res[0] == '1');
+    // column-sum form on edge-incidence LPs (R-23) when the residuals are far larger than the L2
+    // (4 m >= 1 GiB: R-MAT 26; below that the residual form's shorter slack-tile chain wins or
+    // ties, measured on configs 2 and 3).  THETIS_ASYNC_FORM=colsum / residual forces one form
+    // where both apply (same order, same result within rounding: tests run both, A/B timing).
+    const char* env_form = getenv("THETIS_ASYNC_FORM");
+    const bool gd_ok = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr;
+    const bool gd = gd_ok && (env_form && !strcmp(env_form, "colsum")     ? true
+                              : env_form && !strcmp(env_form, "residual") ? false
+                                                                           : 4 * L.m >= ((int64_t)1 << 30));
     // hot prefix: the slots kept in L2 with evict_last (12 B each: x and D), a multiple of 32
 #ifndef THETIS_GD_HOT
 #define THETIS_GD_HOT (1 << 22)
@@ -921,9 +925,10 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     int batch = kPiBatch;
     int64_t window = n_tiles / (step_rule == THETIS_STEP_LJ ? THETIS_PI_DEPTH_LJ : THETIS_PI_DEPTH);
     if (window < 1) window = 1;
-    if (warps * batch > window) {
-        batch = window >= 4 * kPiWarps ? kPiBatch : 1;
-        warps = window / batch;
+    if (warps * batch > window) {  // the window binds: as many warps as fit, each drawing fewer slots at once
+        batch = (int)(window / warps);
+        if (batch < 1) batch = 1;
+        if (warps * batch > window) warps = window / batch;
         if (warps < 1) warps = 1;
     }
     if (serial) {

@@ -112,8 +112,10 @@ def test_alm_det_bit_exact(th, problem):
 
 
 @pytest.mark.gpu
-def test_alm_async_matches_reference(th):
+@pytest.mark.parametrize("form", ["residual", "colsum"])
+def test_alm_async_matches_reference(th, form, monkeypatch):
     import inputs
+    monkeypatch.setenv("THETIS_ASYNC_FORM", form)  # both forms of THETIS_MODE_ASYNC (R-23)
     cfg = inputs.CONFIGS["vc_er_1k"]
     gr = inputs.make_graph(cfg)
     g = th.LP.from_graph(VC, gr.n, gr.src, gr.dst, vertex_w=gr.vertex_w)
@@ -140,9 +142,9 @@ def test_alm_validation(th):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["async", "hublag"])
+@pytest.mark.parametrize("mode", ["async", "async-colsum", "hublag"])
 @pytest.mark.parametrize("problem", [VC, MIS])
-def test_alm_async_serial_matches_replay(th, problem, mode):
+def test_alm_async_serial_matches_replay(th, problem, mode, monkeypatch):
     # anchors through the whole async epoch -- THETIS_MODE_ASYNC (big-tile chunks, slack
     # tiles) or the hub-lag variant (row pass with anchors, hub step, light tiles through
     # lv): the one-tile-in-flight kernels equal the oracle's replays of their schedules
@@ -153,7 +155,8 @@ def test_alm_async_serial_matches_replay(th, problem, mode):
     w = rng.uniform(1, 10, n).astype(np.float32)
     g = th.LP.from_graph(problem, n, src, dst, vertex_w=w)
     r = RefLP.graph(problem, n, src, dst, vertex_w=w)
-    gm, rm = ((th.THETIS_MODE_ASYNC_SERIAL, oracle.MODE_PI_TILE_SYNC) if mode == "async" else
+    monkeypatch.setenv("THETIS_ASYNC_FORM", "colsum" if mode == "async-colsum" else "residual")
+    gm, rm = ((th.THETIS_MODE_ASYNC_SERIAL, oracle.MODE_PI_TILE_SYNC) if mode.startswith("async") else
               (th.THETIS_MODE_ASYNC_HUBLAG_SERIAL, oracle.MODE_HUBLAG_REPLAY))
     st, ub, zb = g.solve_alm(10.0, 2.0, 3, 6, mode=gm, seed=5, target_eps=-1.0)
     rs = r.solve_alm(10.0, 2.0, 3, 6, mode=rm, seed=5, target_eps=-1.0)

@@ -405,31 +405,49 @@ def assert_bj_async(g, r, beta, problem, f_tol=1e-3, cost_tol=1e-2):
     assert o["drift_inf"] < 1e-4 * max(1.0, o["resid_inf"])
 
 
+def async_forms(problem):
+    """the forms THETIS_MODE_ASYNC has on this problem (R-23): VC / MIS run in the
+    residual form and in the column-sum form (same order, same oracle); THETIS_ASYNC_FORM is
+    read by the library at every solve call"""
+    return ["residual", "colsum"] if problem in (VC, MIS) else ["residual"]
+
+
+@pytest.fixture
+def form_env(monkeypatch):
+    def set_form(form):
+        monkeypatch.setenv("THETIS_ASYNC_FORM", form)
+    return set_form
+
+
 @pytest.mark.parametrize("rule", [0, 1])
 @pytest.mark.parametrize("name", ["vc_cfg1", "mis_cfg1", "mwc_grid40", "vc_hubs"])
-def test_async_serial_equals_pi_tile_sync_replay(th, name, rule):
+def test_async_serial_equals_pi_tile_sync_replay(th, name, rule, form_env):
     # THETIS_MODE_ASYNC with one tile in flight is the oracle's mode 4 (the permuted sweep
     # with tile-synchronous scalar / slack units, k-blocks one at a time): the exact
     # arithmetic check of the async kernel (big-tile chunks included: vc_hubs)
     c = async_cases()[name]
-    g = build_case(th, c)
     r = build_case(th, c, bits=64)
-    g.solve(10.0, c["epochs"], mode=th.THETIS_MODE_ASYNC_SERIAL, seed=71, step_rule=rule)
     r.solve(10.0, c["epochs"], mode=oracle.MODE_PI_TILE_SYNC, seed=71, step_rule=rule)
-    assert close(g.get_x().cpu().numpy(), r.x()) and close(g.get_r().cpu().numpy(), r.r())
+    for form in async_forms(c["problem"]):
+        form_env(form)
+        g = build_case(th, c)
+        g.solve(10.0, c["epochs"], mode=th.THETIS_MODE_ASYNC_SERIAL, seed=71, step_rule=rule)
+        assert close(g.get_x().cpu().numpy(), r.x()) and close(g.get_r().cpu().numpy(), r.r()), form
 
 
 @pytest.mark.parametrize("rule", [0, 1])
 @pytest.mark.parametrize("name", ["vc_cfg1", "mis_cfg1", "mwc_grid40", "vc_hubs"])
-def test_async_matches_alg1_trajectory(th, name, rule):
+def test_async_matches_alg1_trajectory(th, name, rule, form_env):
     # THETIS_MODE_ASYNC (Hogwild over the permuted tiles) against Alg. 1 one unit at a time
     # in the same order (oracle MODE_ASYNC, P:373-385), within the BASELINE tolerances
     c = async_cases()[name]
-    g = build_case(th, c)
     r = build_case(th, c, bits=64)
-    g.solve(10.0, c["epochs"], mode=th.THETIS_MODE_ASYNC, seed=71, step_rule=rule)
     r.solve(10.0, c["epochs"], mode=oracle.MODE_ASYNC, seed=71, step_rule=rule)
-    assert_bj_async(g, r, 10.0, c["problem"])
+    for form in async_forms(c["problem"]):
+        form_env(form)
+        g = build_case(th, c)
+        g.solve(10.0, c["epochs"], mode=th.THETIS_MODE_ASYNC, seed=71, step_rule=rule)
+        assert_bj_async(g, r, 10.0, c["problem"])
 
 
 @pytest.mark.parametrize("rule", [0, 1])

@@ -45,6 +45,18 @@ def set_cover_instance(n_elem=1_000_000, n_sets=200_000, mean_extra=4.0, seed=31
     return (n_elem, n_sets, colptr, elem[order].astype(np.int32), rowptr, sets.astype(np.int32), cost)
 
 
+def async_form(mode, prob, m):
+    """the form THETIS_MODE_ASYNC takes (R-23; the library's rule, restated)"""
+    if mode != 1:
+        return None
+    if prob not in (1, 2):
+        return "residual"
+    env = os.environ.get("THETIS_ASYNC_FORM")
+    if env in ("colsum", "residual"):
+        return env
+    return "colsum" if 4 * m >= (1 << 30) else "residual"
+
+
 def main():
     import torch
 
@@ -53,6 +65,7 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
+    ap.add_argument("--modes", default=None, help="comma list of modes to run (0 det, 1 async, 3 hub-lag)")
     a = ap.parse_args()
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
@@ -61,6 +74,8 @@ def main():
     cache = {}
     for name, mode, rule, cap in RUNS:
         if a.only and a.only not in name:
+            continue
+        if a.modes and str(mode) not in a.modes.split(","):
             continue
         prob = PROBLEM[name]
         if name == "sc_1m":
@@ -124,7 +139,7 @@ def main():
                 e1.synchronize()
                 extra["round_" + rname] = dict(ms=e0.elapsed_time(e1), cost=rr["cost"], feasible=rr["feasible"])
             pass  # (lp_obj and eps are in every line)
-        out = dict(config=name, mode=MODE_NAME[mode], step_rule="LJ" if rule else "LMAX", epochs=epochs,
+        out = dict(config=name, form=async_form(mode, prob, lp.m), mode=MODE_NAME[mode], step_rule="LJ" if rule else "LMAX", epochs=epochs,
                    ms_epoch_median=med, eps=ob["max_violation_eps"], lp_obj=ob["lp_obj"],
                    ms_epoch_first=ms[0], updates_per_s=upd / med * 1e3, nnz_per_s=nnz / med * 1e3,
                    alg_bytes_per_epoch=alg, alg_GBps=alg / med / 1e6, frac_of_measured_hbm=alg / med / 1e6 / peak,
