@@ -68,6 +68,8 @@ void destroy(thetis_lp* lp) {
     if (lp->side) cudaStreamDestroy(lp->side);
     if (lp->ev_fork) cudaEventDestroy(lp->ev_fork);
     if (lp->ev_join) cudaEventDestroy(lp->ev_join);
+    for (auto q : lp->det_s) if (q) cudaStreamDestroy(q);
+    for (auto e : lp->det_ev) if (e) cudaEventDestroy(e);
     for (auto e : lp->ev_epoch) cudaEventDestroy(e);
     for (auto e : lp->ev_kern) cudaEventDestroy(e);
     delete lp;

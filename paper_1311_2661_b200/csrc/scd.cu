@@ -52,39 +52,63 @@ __global__ void __launch_bounds__(256) k_det_class(DevLP L, StepParams P, const 
     }
 }
 
-// det: one warp per scalar column with kDetWarpCol < nnz <= kDetCtaCol
+// det: one warp per scalar column with kDetWarpCol < nnz <= kDetCtaCol (= 1024: one entry per
+// virtual lane slot, lane q holds the contract's lanes q + 32 i).  The row words and the r
+// values of the gather stay in registers for the scatter: no unit of the class shares a row,
+// so r_i is still the value read (two dependent round trips per column instead of ten).
 __global__ void __launch_bounds__(256) k_det_mid(DevLP L, StepParams P, const int32_t* __restrict__ cols, int64_t n) {
+    static_assert(kDetCtaCol == 1024, "k_det_mid holds one entry per lane slot");
     const int lane = threadIdx.x & 31;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
     const int64_t j = cols[w];
-    const int64_t beg = L.colptr[j], end = L.colptr[j + 1];
-    const float D = col_dot_tree_warp(L, j, L.r, lane);
-    float z = L.z[j];
-    float g = grad_from(c_int(L, j), ua_of(L, j), D, z, zbar_of(L, j), P.beta);
-    float invL = unit_invL(P, col_norm2(L, j));
-    float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), col_lo(L, j), col_hi(L, j));
-    float d = __fsub_rn(zn, z);
-    if (d != 0.0f)  // the column's rows are distinct: eight read-modify-writes in flight
-        for (int64_t t0 = beg + lane; t0 < end; t0 += 32 * 8) {
-            int64_t row[8];
-            float a[8], rv[8];
+    const int64_t beg = L.colptr[j], len = L.colptr[j + 1] - beg;
+    uint32_t raw[32];
+    float rv[32], p[32];
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const int64_t t = t0 + 32 * q;
-                row[q] = 0;
-                a[q] = 0.0f;
-                if (t < end) entry(L, t, row[q], a[q]);
+    for (int i = 0; i < 32; i++) {
+        const int64_t t = lane + 32 * i;
+        raw[i] = t < len ? (uint32_t)L.rowidx[beg + t] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const int64_t t = lane + 32 * i;
+        rv[i] = t < len ? L.r[raw[i] & kRowMask] : 0.0f;
+    }
+    const float z = L.z[j], cj = c_int(L, j), ua = ua_of(L, j), zb = zbar_of(L, j);
+    const float invL = unit_invL(P, col_norm2(L, j));
+    const float lo = col_lo(L, j), hi = col_hi(L, j);
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const int64_t t = lane + 32 * i;
+        float term = 0.0f;
+        if (t < len) term = L.val ? __fmul_rn(L.val[beg + t], rv[i]) : ((raw[i] & kSignBit) ? -rv[i] : rv[i]);
+        p[i] = t < len ? __fadd_rn(0.0f, term) : 0.0f;
+    }
+#pragma unroll
+    for (int s2 = 16; s2 >= 1; s2 >>= 1)  // off = 512 .. 32: within the lane
+#pragma unroll
+        for (int i = 0; i < s2; i++) p[i] = __fadd_rn(p[i], p[i + s2]);
+    float q = p[0];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {  // off = 16 .. 1: across lanes
+        const float o = __shfl_down_sync(0xffffffffu, q, off);
+        if (lane < off) q = __fadd_rn(q, o);
+    }
+    const float D = __shfl_sync(0xffffffffu, q, 0);
+    const float g = grad_from(cj, ua, D, z, zb, P.beta);
+    const float zn = clamp_lohi(__fsub_rn(z, __fmul_rn(g, invL)), lo, hi);
+    const float d = __fsub_rn(zn, z);
+    if (d != 0.0f) {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int64_t t = lane + 32 * i;
+            if (t < len) {
+                const float ad = L.val ? __fmul_rn(L.val[beg + t], d) : ((raw[i] & kSignBit) ? -d : d);
+                L.r[raw[i] & kRowMask] = __fadd_rn(rv[i], ad);
             }
-#pragma unroll
-            for (int q = 0; q < 8; q++) rv[q] = t0 + 32 * q < end ? L.r[row[q]] : 0.0f;
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                if (t0 + 32 * q < end) {
-                    const float ad = L.val ? __fmul_rn(a[q], d) : (a[q] < 0.0f ? -d : d);
-                    L.r[row[q]] = __fadd_rn(rv[q], ad);
-                }
         }
+    }
     if (lane == 0) L.z[j] = zn;
 }
 
@@ -100,6 +124,20 @@ __global__ void __launch_bounds__(256) k_det_mid(DevLP L, StepParams P, const in
 //   scatter: CTA (column, b): r_i += a_ij d_j over a share of the column's entries
 //            (rows of one class are distinct: plain read-modify-write)
 struct LongBlk { int32_t col, b, nblk; int64_t pbase; };
+// the contract's offsets 2^16 .. 1024 on one 1024-lane slot: with 2^LGB blocks of lanes, the
+// halving p_b += p_{b+h} (h = 2^(LGB-1) .. 1) is the binary tree G(r, 2^LG) = G(r, 2^(LG+1)) +
+// G(r + 2^LG, 2^(LG+1)) over the residues of b, leaves G(r, 2^LGB) = lane value of block r
+// (+0 past the column); Pl points at the slot's value in block 0, blocks are 1024 floats apart
+template <int LG, int LGB>
+__device__ __forceinline__ float tree_b(const float* __restrict__ Pl, int r, int nblk) {
+    if constexpr (LG == LGB) {
+        return r < nblk ? Pl[1024 * (int64_t)r] : 0.0f;
+    } else {
+        const float lo = tree_b<LG + 1, LGB>(Pl, r, nblk);
+        const float hi = tree_b<LG + 1, LGB>(Pl, r + (1 << LG), nblk);
+        return __fadd_rn(lo, hi);
+    }
+}
 __global__ void __launch_bounds__(1024) k_det_long_lanes(DevLP L, const LongBlk* __restrict__ blk, float* __restrict__ Pbuf) {
     const LongBlk B = blk[blockIdx.x];
     const int64_t cb = L.colptr[B.col], len = L.colptr[B.col + 1] - cb;
@@ -113,12 +151,19 @@ __global__ void __launch_bounds__(1024) k_det_long_step(DevLP L, StepParams P, c
     const int l = threadIdx.x, lane = l & 31;
     int lgb = 0;
     while ((1 << lgb) < B.nblk) lgb++;
-    TreeStack ts;
-    for (int bb = 0; bb < (1 << lgb); bb++) {
-        const int b = lgb ? (int)(__brev((unsigned)bb) >> (32 - lgb)) : 0;
-        ts.push(b < B.nblk ? Pbuf[B.pbase + 1024 * (int64_t)b + l] : 0.0f);
+    const float* Pl = Pbuf + B.pbase + l;
+    float comb;
+    switch (lgb) {  // the tree over b fully unrolled per depth: loads independent, partial sums in registers
+        case 0: comb = tree_b<0, 0>(Pl, 0, B.nblk); break;
+        case 1: comb = tree_b<0, 1>(Pl, 0, B.nblk); break;
+        case 2: comb = tree_b<0, 2>(Pl, 0, B.nblk); break;
+        case 3: comb = tree_b<0, 3>(Pl, 0, B.nblk); break;
+        case 4: comb = tree_b<0, 4>(Pl, 0, B.nblk); break;
+        case 5: comb = tree_b<0, 5>(Pl, 0, B.nblk); break;
+        case 6: comb = tree_b<0, 6>(Pl, 0, B.nblk); break;
+        default: comb = tree_b<0, 7>(Pl, 0, B.nblk); break;
     }
-    sp[l] = ts.st[0];
+    sp[l] = comb;
     __syncthreads();
     for (int off = 512; off >= 32; off >>= 1) {
         if (l < off) sp[l] = __fadd_rn(sp[l], sp[l + off]);
@@ -1145,18 +1190,38 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     // det: one epoch = the class launches (identical every epoch), captured once into a
     // CUDA graph (on the side stream) and replayed per epoch: a launch-bound epoch on small
     // LPs pays one graph launch instead of K + 1 kernel launches
-    auto det_epoch = [&](cudaStream_t q) {
+    // fork = true (graph capture only): a class's thread columns, warp columns and CTA columns
+    // are independent (units of a class share no row), so they are captured as three parallel
+    // branches and joined before the next class
+    auto det_epoch = [&](cudaStream_t q, bool fork) {
         for (int64_t c = 0; c < lp->K; c++) {
             int64_t beg = lp->class_ptr[c], cnt = lp->class_ptr[c + 1] - beg;
-            if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
-            else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
             const int64_t nm = mid_ptr[c + 1] - mid_ptr[c], nl = long_ptr[c + 1] - long_ptr[c];
             const int64_t nb = lblk_ptr[c + 1] - lblk_ptr[c];
-            if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, q>>>(L, P, mid_cols + mid_ptr[c], nm);
+            const bool f = fork && (nm > 0 || nl > 0);
+            cudaStream_t qm = f ? lp->det_s[0] : q, ql = f ? lp->det_s[1] : q;
+            if (f) {
+                cudaEventRecord(lp->det_ev[0], q);
+                if (nm > 0) cudaStreamWaitEvent(qm, lp->det_ev[0], 0);
+                if (nl > 0) cudaStreamWaitEvent(ql, lp->det_ev[0], 0);
+            }
+            if (cnt > 0 && L.k <= 8) k_det_class<8><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
+            else if (cnt > 0) k_det_class<kMaxK><<<grid_for(cnt, 256, 1 << 30), 256, 0, q>>>(L, P, lp->members + beg, cnt);
+            if (nm > 0) k_det_mid<<<grid_for(32 * nm, 256, 1 << 30), 256, 0, qm>>>(L, P, mid_cols + mid_ptr[c], nm);
             if (nl > 0) {
-                k_det_long_lanes<<<(unsigned)nb, 1024, 0, q>>>(L, lblk + lblk_ptr[c], Pbuf);
-                k_det_long_step<<<(unsigned)nl, 1024, 0, q>>>(L, P, lcols + long_ptr[c], Pbuf, dcol);
-                k_det_long_scatter<<<(unsigned)nb, 1024, 0, q>>>(L, lblk + lblk_ptr[c], lblk_col + lblk_ptr[c], dcol);
+                k_det_long_lanes<<<(unsigned)nb, 1024, 0, ql>>>(L, lblk + lblk_ptr[c], Pbuf);
+                k_det_long_step<<<(unsigned)nl, 1024, 0, ql>>>(L, P, lcols + long_ptr[c], Pbuf, dcol);
+                k_det_long_scatter<<<(unsigned)nb, 1024, 0, ql>>>(L, lblk + lblk_ptr[c], lblk_col + lblk_ptr[c], dcol);
+            }
+            if (f) {
+                if (nm > 0) {
+                    cudaEventRecord(lp->det_ev[1], qm);
+                    cudaStreamWaitEvent(q, lp->det_ev[1], 0);
+                }
+                if (nl > 0) {
+                    cudaEventRecord(lp->det_ev[2], ql);
+                    cudaStreamWaitEvent(q, lp->det_ev[2], 0);
+                }
             }
         }
         if (L.n_ineq > 0) k_det_slacks<<<grid_for(L.n_ineq, 256), 256, 0, q>>>(L, P);
@@ -1171,8 +1236,14 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
     cudaGraphExec_t det_graph = nullptr;
     if (mode == THETIS_MODE_DETERMINISTIC && epochs > 1 && lp->side) {
         cudaGraph_t g = nullptr;
+        bool fork = true;  // the branch streams and events of the capture (created once per handle)
+        for (auto& q : lp->det_s)
+            if (!q && cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) != cudaSuccess) fork = false;
+        for (auto& ev : lp->det_ev)
+            if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) fork = false;
+        cudaGetLastError();
         if (cudaStreamBeginCapture(lp->side, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-            det_epoch(lp->side);
+            det_epoch(lp->side, fork);
             if (cudaStreamEndCapture(lp->side, &g) == cudaSuccess && g) {
                 if (cudaGraphInstantiate(&det_graph, g, 0) != cudaSuccess) det_graph = nullptr;
                 lp->det_graph = det_graph;  // owned by the handle from here (released on every path)
@@ -1187,7 +1258,7 @@ int solve_epochs(thetis_lp* lp, float beta, int epochs, int mode, uint64_t seed,
         NvtxRange nvtx_(mode == THETIS_MODE_DETERMINISTIC ? "det epoch" : "hub-lag epoch");
         if (mode == THETIS_MODE_DETERMINISTIC) {
             if (det_graph) CUDA_TRY(lp, cudaGraphLaunch(det_graph, s));
-            else det_epoch(s);
+            else det_epoch(s, false);
         } else {
             // (1) hub step + (2) slack sweep, fused; or (2) alone
             if (H.n_heavy > 0) {

@@ -10,7 +10,9 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int64_t kDetWarpCol = 32;  // det: columns longer than this use the warp path
-constexpr int64_t kDetCtaCol = 8192; // ... and longer than this a CTA per 1024 contract lanes (k_det_long_*)
+constexpr int64_t kDetCtaCol = 1024; // ... and longer than this a CTA per 1024 contract lanes (k_det_long_*);
+                                     // (8192 until round 2: a warp walking an 8192-entry column took ~0.12 ms per
+                                     // class on config 3, 344 classes per epoch)
 
 struct StepParams {
     float beta;       // caller's beta

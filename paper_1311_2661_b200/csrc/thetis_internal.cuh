@@ -324,6 +324,8 @@ struct thetis_lp {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // second stream: hub-hub row pass beside the light tiles
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t det_s[2] = {nullptr, nullptr};  // branches of a captured det class (warp columns, CTA columns)
+    cudaEvent_t det_ev[3] = {nullptr, nullptr, nullptr};
     cudaGraphExec_t det_graph = nullptr;  // the last deterministic solve's epoch graph
     std::vector<cudaEvent_t> ev_epoch;
     std::vector<cudaEvent_t> ev_kern;   // per-kernel marks of timed async epochs
