@@ -189,6 +189,8 @@ __device__ __forceinline__ int2 ld_cs_int2(const int2* p) {  // streamed once pe
     return v;
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // the tile's scalar columns: lanes [a, b), first column j0
 __device__ __forceinline__ TileCols tile_cols(const DevLP& L, int64_t tile) {
     TileCols tc;
@@ -372,6 +374,19 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
     if (kBlocks && tile * 32 < L.n_blocks) {
         const int nb = (int)(L.n_blocks - tile * 32 < 32 ? L.n_blocks - tile * 32 : 32);
         unsigned live = __ballot_sync(0xffffffffu, lane < nb && !(L.unit_fixed && L.unit_fixed[u]));
+        // the blocks step one after the other, each a chain column starts -> row words -> r -> step:
+        // bring the tile's static data (one contiguous CSC range, its column starts, values and
+        // costs) into L1 once, so that only the read of r is a long round trip per block
+        {
+            const int64_t c0 = tile * 32 * L.k, c1 = c0 + (int64_t)nb * L.k;
+            const int64_t rb = L.colptr[c0], re = L.colptr[c1];
+            for (int64_t q = c0 + 16 * lane; q <= c1; q += 16 * 32) prefetch_l1(L.colptr + q);
+            for (int64_t q = c0 + 32 * lane; q < c1; q += 32 * 32) {
+                prefetch_l1(L.z + q);
+                prefetch_l1(L.c + q);
+            }
+            for (int64_t t = rb + 32 * lane; t < re; t += 32 * 32) prefetch_l1(L.rowidx + t);
+        }
         while (live) {
             const int i = __ffs(live) - 1;
             live &= live - 1;
