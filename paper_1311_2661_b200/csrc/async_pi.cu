@@ -829,15 +829,27 @@ __global__ void k_vindex(const int64_t* ev_vstart, int64_t n_ev, const int64_t* 
 
 }  // namespace
 
-// window: at most ~n_tiles / depth tiles in flight (bounded staleness); the
-// depth depends on the step rule: 1/L_j steps are up to max_j ||a_j||^2 times longer than
-// 1/L_max's, and the admissible number of concurrent updaters "depends on ... the diagonal
-// dominance properties of the Hessian"; values measured in DESIGN.md R-6
+// window: at most n_tiles / depth slots drawn and unfinished (bounded staleness),
+// filled with as many warps as fit (each warp works on one tile at a time and draws
+// window / warps slots at once).  The depth depends on the step rule -- 1/L_j steps are up to
+// max_j ||a_j||^2 times longer than 1/L_max's, and the admissible number of concurrent
+// updaters "depends on ... the diagonal dominance properties of the Hessian" -- and
+// on the form: the residual form delays a big tile's scatter behind its gather and steps
+// coupled simplex blocks, and needs a window a quarter as wide as the column-sum form, whose
+// hub sums are always current.  Values measured against Alg. 1 (R-6): R-MAT 22 under
+// 1/L_max with n_tiles / 512 slots: residual form 1.2e-3 off in c^T x, column-sum form 3.1e-4;
+// config 4 at full size (MWC): rounded cut 2% off with n_tiles / 1024, inside 1% with / 2048.
 #ifndef THETIS_PI_DEPTH
-#define THETIS_PI_DEPTH 512
+#define THETIS_PI_DEPTH 2048
 #endif
 #ifndef THETIS_PI_DEPTH_LJ
-#define THETIS_PI_DEPTH_LJ 4096
+#define THETIS_PI_DEPTH_LJ 16384
+#endif
+#ifndef THETIS_PI_DEPTH_GD
+#define THETIS_PI_DEPTH_GD 512
+#endif
+#ifndef THETIS_PI_DEPTH_GD_LJ
+#define THETIS_PI_DEPTH_GD_LJ 4096
 #endif
 
 int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool serial, uint64_t seed,
@@ -853,15 +865,11 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     const int64_t n_tiles = (L.U + 31) / 32;
     const int64_t n_struct = L.n_blocks + L.n_scalar;
     const int64_t n_struct_tiles = (n_struct + 31) / 32;
-    // column-sum form on edge-incidence LPs (R-23) when the residuals are far larger than the L2
-    // (4 m >= 1 GiB: R-MAT 26; below that the residual form's shorter slack-tile chain wins or
-    // ties, measured on configs 2 and 3).  THETIS_ASYNC_FORM=colsum / residual forces one form
-    // where both apply (same order, same result within rounding: tests run both, A/B timing).
+    // column-sum form on edge-incidence LPs (R-23).  THETIS_ASYNC_FORM=residual keeps the
+    // residual form there too (same order, same result within rounding: tests run both, A/B timing)
     const char* env_form = getenv("THETIS_ASYNC_FORM");
     const bool gd_ok = (L.problem == THETIS_PROB_VC || L.problem == THETIS_PROB_MIS) && lp->nbr && L.val == nullptr;
-    const bool gd = gd_ok && (env_form && !strcmp(env_form, "colsum")     ? true
-                              : env_form && !strcmp(env_form, "residual") ? false
-                                                                           : 4 * L.m >= ((int64_t)1 << 30));
+    const bool gd = gd_ok && !(env_form && !strcmp(env_form, "residual"));
     // hot prefix: the slots kept in L2 with evict_last (12 B each: x and D), a multiple of 32
 #ifndef THETIS_GD_HOT
 #define THETIS_GD_HOT (1 << 22)
@@ -938,7 +946,8 @@ int solve_async_pi(thetis_lp* lp, float beta, int step_rule, int epochs, bool se
     if (per_sm < 1) per_sm = 1;
     int64_t warps = (int64_t)per_sm * sms * kPiWarps;
     int batch = kPiBatch;
-    int64_t window = n_tiles / (step_rule == THETIS_STEP_LJ ? THETIS_PI_DEPTH_LJ : THETIS_PI_DEPTH);
+    int64_t window = n_tiles / (gd ? (step_rule == THETIS_STEP_LJ ? THETIS_PI_DEPTH_GD_LJ : THETIS_PI_DEPTH_GD)
+                                   : (step_rule == THETIS_STEP_LJ ? THETIS_PI_DEPTH_LJ : THETIS_PI_DEPTH));
     if (window < 1) window = 1;
     if (warps * batch > window) {  // the window binds: as many warps as fit, each drawing fewer slots at once
         batch = (int)(window / warps);

@@ -53,6 +53,8 @@ def main():
     ap.add_argument("--rules", default="0,1")
     ap.add_argument("--epochs", type=int, default=0)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--forms", default="auto", help="THETIS_ASYNC_FORM values for mode 1 on VC / MIS: "
+                                                    "auto (the library's rule), residual, colsum")
     a = ap.parse_args()
     cache = json.load(open(CACHE)) if os.path.exists(CACHE) else {}
     for case in a.cases.split(","):
@@ -75,14 +77,22 @@ def main():
                 json.dump(cache, open(CACHE, "w"))
                 print(f"{case} rule {rule} oracle f={base[0]:.9e} cx={base[1]:.9e} cost={base[2]:.9e} "
                       f"({time.time() - t0:.1f}s)", flush=True)
+            runs = []
             for mode in [int(x) for x in a.modes.split(",")]:
+                forms = a.forms.split(",") if mode == 1 and cfg.problem in (1, 2) else ["auto"]
+                runs += [(mode, f) for f in forms]
+            for mode, form in runs:
+                if form == "auto":
+                    os.environ.pop("THETIS_ASYNC_FORM", None)
+                else:
+                    os.environ["THETIS_ASYNC_FORM"] = form
                 lp = th.LP.from_graph(cfg.problem, g.n, g.src, g.dst, device="cuda:0", **kw)
                 st = lp.solve(cfg.beta, ep, mode=mode, seed=cfg.solve_seed, step_rule=rule)
                 o = lp.objective(cfg.beta)
                 _, rr = lp.round(rule_round(cfg), seed=cfg.round_seed)
                 v = (o["f_beta"], o["lp_obj"], rr["cost"])
                 ms = np.median(st["ms_per_epoch"]) if st["ms_per_epoch"] else 0.0
-                msg = f"{case} rule {rule} mode {mode} f={v[0]:.9e} cx={v[1]:.9e} cost={v[2]:.9e} ms/epoch={ms:.3f}"
+                msg = f"{case} rule {rule} mode {mode} form {form} f={v[0]:.9e} cx={v[1]:.9e} cost={v[2]:.9e} ms/epoch={ms:.3f}"
                 if base:
                     d = [(v[i] - base[i]) / abs(base[i]) if base[i] else 0.0 for i in range(3)]
                     msg += f" | df={d[0]:+.2e} dcx={d[1]:+.2e} dcost={d[2]:+.2e} drift={o['drift_inf']:.1e}"

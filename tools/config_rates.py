@@ -51,10 +51,7 @@ def async_form(mode, prob, m):
         return None
     if prob not in (1, 2):
         return "residual"
-    env = os.environ.get("THETIS_ASYNC_FORM")
-    if env in ("colsum", "residual"):
-        return env
-    return "colsum" if 4 * m >= (1 << 30) else "residual"
+    return "residual" if os.environ.get("THETIS_ASYNC_FORM") == "residual" else "colsum"
 
 
 def main():

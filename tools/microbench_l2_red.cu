@@ -1,4 +1,6 @@
-// microbenchmark: random fp32 RED into an L2-resident array; coalesced streaming read
+// microbenchmark: random fp32 / fp64 RED into an L2-resident array (22 MB, 48 MB: the hot set of
+// the column-sum async form); coalesced streaming read.  Reference rates for the RED sector
+// counts in profiles/*ncu*: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/microbench_l2_red.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -7,6 +9,13 @@ __global__ void k_red(float* acc, int64_t n_acc, int64_t ops, uint64_t seed, int
     for (int64_t i = tid; i < ops; i += nt) {
         uint64_t h = (i + seed) * 0x9E3779B97F4A7C15ULL; h ^= h >> 29; h *= 0xBF58476D1CE4E5B9ULL; h ^= h >> 32;
         atomicAdd(acc + (h % n_acc), 1.0f);
+    }
+}
+__global__ void k_red64(double* acc, int64_t n_acc, int64_t ops, uint64_t seed) {
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < ops; i += nt) {
+        uint64_t h = (i + seed) * 0x9E3779B97F4A7C15ULL; h ^= h >> 29; h *= 0xBF58476D1CE4E5B9ULL; h ^= h >> 32;
+        atomicAdd(acc + (h % n_acc), 1.0);
     }
 }
 __global__ void k_stream(const float4* a, int64_t n, float* out) {
@@ -25,6 +34,14 @@ int main() {
             cudaEventRecord(e0); k_red<<<blocks, 256>>>(acc, n_acc, ops, it, 1); cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             printf("red random 22MB: blocks %d  %.2f ms  %.1f G/s\n", blocks, ms, ops / ms / 1e6);
+        }
+        for (int64_t mb : {22, 48}) {
+            const int64_t n64 = (mb << 20) >> 3;
+            double* acc64; cudaMalloc(&acc64, n64 * 8); cudaMemset(acc64, 0, n64 * 8);
+            cudaEventRecord(e0); k_red64<<<148 * 32, 256>>>(acc64, n64, ops, it); cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms64; cudaEventElapsedTime(&ms64, e0, e1);
+            printf("red.f64 random %lld MB: blocks %d  %.2f ms  %.1f G/s\n", (long long)mb, 148 * 32, ms64, ops / ms64 / 1e6);
+            cudaFree(acc64);
         }
         cudaEventRecord(e0); k_stream<<<148 * 8, 256>>>((float4*)a, big / 16, acc); cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
