@@ -98,6 +98,19 @@ def algorithmic_bytes(n_s, nnz_s, m):
     return 20 * n_s + 12 * nnz_s + 16 * m
 
 
+def ncu_summary():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# random RED rate into an L2-resident array on this part (tools/microbench_l2_red.cu,
+# profiles/r02_l2_red_microbench.txt: 220 G/s for fp32 and fp64, 22 MB and 48 MB arrays)
+L2_RED_PEAK_GOPS = 220.0
+
+
 def ncu_traffic():
     """DRAM bytes of one SCD epoch (its kernels' dram__bytes_read.sum + dram__bytes_write.sum)
     from the committed ncu summary (tools/profile_round.sh + tools/ncu_summary.py), or None"""
@@ -107,6 +120,18 @@ def ncu_traffic():
             return json.load(f).get("epoch_dram_bytes")
     except Exception:
         return None
+
+
+def l2_ops(ep_ms):
+    sm = ncu_summary()
+    red, rd = sm.get("l2_red_sectors"), sm.get("l2_read_sectors")
+    if not red or not rd:
+        return None
+    return {"bound": "l2 random sector operations (atomics)", "red_sectors": red, "read_sectors": rd,
+            "achieved_red_Gops": red / ep_ms / 1e6, "achieved_all_Gops": (red + rd) / ep_ms / 1e6,
+            "peak_red_Gops": L2_RED_PEAK_GOPS, "frac_red": red / ep_ms / 1e6 / L2_RED_PEAK_GOPS,
+            "source": "sector counts: profiles/ncu_summary.json (one k_async_pi launch under ncu --set full); peak: "
+                      "tools/microbench_l2_red.cu on this pool (profiles/r02_l2_red_microbench.txt); time: this run"}
 
 
 class Clocks:
@@ -348,7 +373,11 @@ def run_thetis(args):
                      "kernel": "k_async_pi<kGD>: one SCD epoch of THETIS_MODE_ASYNC in column-sum form (one launch per "
                                "epoch; CUDA events around each epoch on the launching stream; SURVEY 8(d) bytes "
                                "per epoch)",
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # the kernel is not DRAM-bound: its epoch is set by random L2 sector operations
+                     # (one RED per structural nonzero into the column sums + the slack tiles' reads
+                     # of x).  Sector counts from the committed ncu capture, time live.
+                     "l2_ops": l2_ops(ep_med)},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),
                    "selected": int(rr.n_selected)},

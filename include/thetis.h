@@ -209,11 +209,10 @@ THETIS_API int thetis_get_r(const thetis_lp* lp, float* dst, int64_t count);
  *  THETIS_MODE_ASYNC: tiles of 32 units in a per-epoch keyed permutation
  *    (R-6), processed concurrently Hogwild-style with atomic
  *    updates, a bounded window of tiles in flight.  Generic LPs and MWC keep the
- *    residual r current (red.global.add.f32); large VC / MIS LPs (4 m >= 1 GiB) keep
- *    the column sums A^T r current instead (fp64; R-23) and recompute
- *    r = A z - b before returning: same order, same result within rounding.  The
- *    environment variable THETIS_ASYNC_FORM=colsum|residual (read at every call)
- *    forces one form on VC / MIS.
+ *    residual r current (red.global.add.f32); VC / MIS LPs keep the column sums
+ *    A^T r current instead (fp64; R-23) and recompute r = A z - b before
+ *    returning: same order, same result within rounding.  The environment variable
+ *    THETIS_ASYNC_FORM=residual (read at every call) keeps the residual form there.
  *  THETIS_MODE_ASYNC_SERIAL: the async kernel with a single tile in flight,
  *    i.e. the tile-synchronous replay of the permutation (diagnostic / tests).
  * seed keys the colouring (det) or the permutations (async).  stats (host)

@@ -94,8 +94,15 @@ def full(rep, out, summary=None):
     if summary:
         rb = float(get["dram__bytes_read.sum"][1].replace(",", "")) * (1e9 if get["dram__bytes_read.sum"][0] == "Gbyte" else 1)
         wb = float(get["dram__bytes_write.sum"][1].replace(",", "")) * (1e9 if get["dram__bytes_write.sum"][0] == "Gbyte" else 1)
+        def num(key):
+            return float(get[key][1].replace(",", "")) if key in get and get[key][1] not in ("", "n/a") else None
         json.dump({"kernel": name, "epoch_dram_bytes": rb + wb, "dram_read_bytes": rb, "dram_write_bytes": wb,
-                   "source": rep, "note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch (= one epoch)"},
+                   "l2_read_sectors": num("lts__t_sectors_srcunit_tex_op_read.sum"),
+                   "l2_red_sectors": num("lts__t_sectors_srcunit_tex_op_red.sum"),
+                   "l2_hit_rate_pct": num("lts__t_sector_hit_rate.pct"),
+                   "duration_ms": num("gpu__time_duration.sum"),
+                   "source": rep, "note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch (= one epoch); "
+                                          "L2 sectors by operation of the same launch"},
                   open(summary, "w"), indent=1)
 
 
