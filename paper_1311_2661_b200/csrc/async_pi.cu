@@ -150,6 +150,13 @@ __device__ __forceinline__ float ld_x_slot(const float* xr, int slot, const L2Po
 #ifndef THETIS_GD_DTYPE
 #define THETIS_GD_DTYPE 0
 #endif
+// THETIS_GD_PULL 1 (default): a vertex forms D_u = deg_u (x_u - 1) + sum_w x_w + S_u at its turn
+// from its neighbours' x (random *reads*, one per nonzero) and the maintained slack sum
+// S_u = sum_i sigma_i s_i (REDs only when a slack moves).  0: D_u itself is maintained, every
+// step pushed into the neighbours' D (one RED per nonzero; the L2's RED rate is 220 G/s)
+#ifndef THETIS_GD_PULL
+#define THETIS_GD_PULL 1
+#endif
 __device__ __forceinline__ void red_D_slot(double* Dg, int slot, double v, const L2Pol& pol) {
     if (THETIS_GD_EXP & 1) return;
     if ((THETIS_GD_EXP & 4) && slot >= pol.hot) return;
@@ -240,6 +247,52 @@ __device__ __forceinline__ void slack_lane_gd(const DevLP& L, const StepParams& 
         red_D_slot(C.Dg, e.x, dr, pol);
         red_D_slot(C.Dg, e.y, dr, pol);
     }
+}
+// X_col += x_w over the neighbours w of the tile's columns, nonzero range [c0, c1), into sm.acc
+// (sub-chunks of 32 inside one column accumulate in registers, mixed ones add per lane)
+__device__ __forceinline__ void gather_x_range(const PiCtx& C, const L2Pol& pol, WarpSmem& sm, int ncols, int64_t c0,
+                                               int64_t c1, int lane) {
+    constexpr int U = 4;
+    int c = col_of(sm, ncols, c0);
+    int64_t nb = sm.cp[c + 1];
+    float acc = 0.0f;
+    for (int64_t b0 = c0; b0 < c1; b0 += 32 * U) {
+        int32_t w[U];
+        float v[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t t = b0 + 32 * q + lane;
+            w[q] = t < c1 ? ld_cs_i32(C.nbr + t) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) v[q] = b0 + 32 * q + lane < c1 ? ld_x_slot(C.xr, w[q], pol) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t base = b0 + 32 * q;
+            if (base >= c1) break;
+            if (nb <= base) {
+                acc = warp_sum(acc);
+                if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
+                acc = 0.0f;
+                do { c++; nb = sm.cp[c + 1]; } while (nb <= base);
+            }
+            const int64_t t = base + lane;
+            if (base + 32 <= nb || c1 <= nb) {
+                acc += v[q];
+            } else if (t < c1 && v[q] != 0.0f) {
+                int col = c;
+                while (sm.cp[col + 1] <= t) col++;
+                atomicAdd(&sm.acc[col], v[q]);
+            }
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0 && acc != 0.0f) atomicAdd(&sm.acc[c], acc);
+    __syncwarp();
+}
+// D_u of the pull form from the column's degree, its x, the gathered neighbour sum and S_u
+__device__ __forceinline__ float pull_D(int64_t deg, float z, float X, double S) {
+    return (float)((double)deg * ((double)z - 1.0) + (double)X + S);
 }
 // D_v += d_col for the neighbours v of the tile's columns over the nonzero range [c0, c1)
 __device__ __forceinline__ void push_range(const PiCtx& C, const L2Pol& pol, WarpSmem& sm, int ncols, int64_t c0,
@@ -419,7 +472,29 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         cj = __shfl_sync(0xffffffffu, cj, (lane + tc.a) & 31);
         float D = 0.0f;
         int rk = 0;
-        if (kGD) {  // column-sum form: D_j is kept current (lane = column index)
+        if (kGD && THETIS_GD_PULL) {  // pull form: the neighbours' x, then D from it (lane = column index)
+            float X = 0.0f;
+            if (lane_path) {
+                for (int64_t q0 = cb; q0 < ce; q0 += 8) {
+                    int32_t w[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) w[q] = q0 + q < ce ? C.nbr[q0 + q] : 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        if (q0 + q < ce) X += ld_x_slot(C.xr, w[q], pol);
+                }
+                X = __shfl_sync(0xffffffffu, X, (lane + tc.a) & 31);
+            } else {
+                sm.acc[lane] = 0.0f;
+                __syncwarp();
+                gather_x_range(C, pol, sm, tc.ncols, beg, end, lane);
+                X = sm.acc[lane];
+            }
+            if (lane < tc.ncols) {
+                rk = C.rank[tc.j0 + lane];
+                D = pull_D(sm.cp[lane + 1] - sm.cp[lane], z, X, ld_cg_f64(C.Dg + rk));
+            }
+        } else if (kGD) {  // push form: D_j is kept current
             if (lane < tc.ncols) {
                 rk = C.rank[tc.j0 + lane];
                 D = ld_D_slot(C.Dg, rk);
@@ -449,12 +524,12 @@ __device__ void process_tile_pi(const DevLP& L, const StepParams& P, const PiCtx
         // x by rank, and the column's own sum: D_j += ||a_j||^2 d_j (||a_j||^2 = its nonzero count)
         if (kGD && d != 0.0f) {
             C.xr[rk] = L.z[tc.j0 + lane];
-            red_D_slot(C.Dg, rk, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d, pol);
+            if (!THETIS_GD_PULL) red_D_slot(C.Dg, rk, (double)(sm.cp[lane + 1] - sm.cp[lane]) * (double)d, pol);
         }
     }
     __syncwarp();
-    // scatters
-    if (moved) {
+    // scatters (none in the pull form: a step is visible through x)
+    if (moved && !(kGD && THETIS_GD_PULL)) {
         if (kGD) {
             if (lane_path) {
                 const int cl = lane - tc.a;
@@ -506,7 +581,35 @@ __device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, 
     PiJob& J = C.jobs[b];
     if (c == 0) process_tile_pi<kBlocks, KC, kGD>(L, P, C, pol, J.tile, sm, lane, false);  // its other units
     const TileCols tc = tile_cols(L, J.tile);
-    if (kGD) {  // column-sum form: nothing to gather; the first chunk's slot takes the tile's steps
+    if (kGD && THETIS_GD_PULL) {  // pull form: partial neighbour sums of x; the last chunk takes the steps
+        load_cp(L, tc, sm, lane);
+        sm.acc[lane] = 0.0f;
+        __syncwarp();
+        const int64_t c0 = J.cb + (int64_t)c * kJobChunk;
+        const int64_t c1 = c0 + kJobChunk < J.ce ? c0 + kJobChunk : J.ce;
+        gather_x_range(C, pol, sm, tc.ncols, c0, c1, lane);
+        if (lane < tc.ncols && sm.acc[lane] != 0.0f) atomicAdd(&J.acc[lane], sm.acc[lane]);
+        __syncwarp();
+        int g = 0;
+        if (lane == 0) g = atom_add_release(&J.gdone, 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g != J.n_chunks - 1) return;
+        if (lane == 0) (void)ld_acquire_u32((const uint32_t*)&J.gdone);
+        __syncwarp();
+        const float X = ld_cg(&J.acc[lane]);
+        float D = 0.0f, z = 0.0f, cj = 0.0f;
+        int rk = 0;
+        if (lane < tc.ncols) {
+            rk = C.rank[tc.j0 + lane];
+            z = L.z[tc.j0 + lane];
+            cj = c_int(L, tc.j0 + lane);
+            D = pull_D(sm.cp[lane + 1] - sm.cp[lane], z, X, ld_cg_f64(C.Dg + rk));
+        }
+        const float d = scalar_step(L, P, tc, D, lane, z, cj);
+        if (d != 0.0f) C.xr[rk] = L.z[tc.j0 + lane];
+        return;
+    }
+    if (kGD) {  // push form: nothing to gather; the first chunk's slot takes the tile's steps
         if (c != 0) return;
         load_cp(L, tc, sm, lane);
         float D = 0.0f, z = 0.0f, cj = 0.0f;
@@ -554,6 +657,7 @@ __device__ void job_gather(const DevLP& L, const StepParams& P, const PiCtx& C, 
 // scatter chunk c of big tile b, whose steps are ready
 template <bool kGD>
 __device__ void job_scatter(const DevLP& L, const PiCtx& C, const L2Pol& pol, int32_t b, int c, WarpSmem& sm, int lane) {
+    if (kGD && THETIS_GD_PULL) return;  // pull form: a big tile's steps are visible through x
     const PiJob& J = C.jobs[b];
     if (lane == 0) (void)ld_acquire_u32(&J.ready);  // the steps and z written before `ready`
     __syncwarp();
@@ -662,7 +766,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, kBlocks ? 3 : kGD ? THETIS_PI_M
                 const int ci = __shfl_sync(0xffffffffu, c, i);
                 if (ki == 1) {
                     job_gather<kBlocks, KC, kGD>(L, P, C, pol, bi, ci, sm, lane);
-                } else if (job_ready(C, bi, lane)) {
+                } else if ((kGD && THETIS_GD_PULL) || job_ready(C, bi, lane)) {
                     job_scatter<kGD>(L, C, pol, bi, ci, sm, lane);
                 } else {  // not ready: keep it (wait only when the list is full)
                     if (df.n == kDefer) run_deferred<kGD>(L, C, pol, df, sm, lane, true);
@@ -736,7 +840,14 @@ __global__ void k_init_colsum(DevLP L, const int2* __restrict__ erank, double* _
     const L2Pol pol = make_l2pol(hot);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.m; i += (int64_t)gridDim.x * blockDim.x) {
         const int2 e = ld_cs_int2(erank + i);
-        const double rv = (double)ld_cs_f32(L.r + i);
+        // push form: D = A^T r (r_i into both endpoints); pull form: S = sum of sigma_i s_i
+        double rv;
+        if (THETIS_GD_PULL) {
+            const float sl = ld_cs_f32(L.z + L.n_s + i);
+            rv = (double)(row_sigma(L, i) < 0.0f ? -sl : sl);
+        } else {
+            rv = (double)ld_cs_f32(L.r + i);
+        }
         if (rv != 0.0) {
             red_D_slot(Dg, e.x, rv, pol);
             red_D_slot(Dg, e.y, rv, pol);
