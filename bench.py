@@ -109,6 +109,8 @@ def ncu_summary():
 # random RED rate into an L2-resident array on this part (tools/microbench_l2_red.cu,
 # profiles/r02_l2_red_microbench.txt: 220 G/s for fp32 and fp64, 22 MB and 48 MB arrays)
 L2_RED_PEAK_GOPS = 220.0
+# random ld.global.cg.f32 rate from an L2-resident array, same microbenchmark
+L2_READ_PEAK_GOPS = 255.0
 
 
 def ncu_traffic():
@@ -125,12 +127,13 @@ def ncu_traffic():
 def l2_ops(ep_ms):
     sm = ncu_summary()
     red, rd = sm.get("l2_red_sectors"), sm.get("l2_read_sectors")
-    if not red or not rd:
+    if red is None or not rd:
         return None
-    return {"bound": "l2 random sector operations (atomics)", "red_sectors": red, "read_sectors": rd,
-            "achieved_red_Gops": red / ep_ms / 1e6, "achieved_all_Gops": (red + rd) / ep_ms / 1e6,
-            "peak_red_Gops": L2_RED_PEAK_GOPS, "frac_red": red / ep_ms / 1e6 / L2_RED_PEAK_GOPS,
-            "source": "sector counts: profiles/ncu_summary.json (one k_async_pi launch under ncu --set full); peak: "
+    return {"bound": "l2 random 32-byte sector operations (reads of x; REDs when slacks move)",
+            "read_sectors": rd, "red_sectors": red, "achieved_Gsectors_per_s": (red + rd) / ep_ms / 1e6,
+            "peak_read_Gsectors_per_s": L2_READ_PEAK_GOPS, "peak_red_Gsectors_per_s": L2_RED_PEAK_GOPS,
+            "frac_of_read_peak": (red + rd) / ep_ms / 1e6 / L2_READ_PEAK_GOPS,
+            "source": "sector counts: profiles/ncu_summary.json (one k_async_pi launch under ncu --set full); peaks: "
                       "tools/microbench_l2_red.cu on this pool (profiles/r02_l2_red_microbench.txt); time: this run"}
 
 
@@ -357,7 +360,7 @@ def run_thetis(args):
         "config": {"workload": f"{CFG_NAME}: VC LP of R-MAT scale {p['scale']} ({E} edge samples, a,b,c = "
                                f"{p['a']},{p['b']},{p['c']}), weights U[1,10), beta {BETA}, {EPOCHS} async "
                                "epochs (THETIS_MODE_ASYNC: Alg. 1's permuted sweep, Hogwild, column-sum form "
-                               "R-23; STEP_LMAX), VC_HALF rounding",
+                               "R-23 (pull); STEP_LMAX), VC_HALF rounding",
                    "step": "build + 20 SCD epochs + reductions + rounding",
                    "vertices": n, "unique_edges_rows": int(dims.m), "coordinates": int(dims.N),
                    "nnz_struct": int(dims.nnz_struct), "l2": "inputs (8.6 GB edge list) and state exceed the L2",
@@ -374,9 +377,9 @@ def run_thetis(args):
                                "epoch; CUDA events around each epoch on the launching stream; SURVEY 8(d) bytes "
                                "per epoch)",
                      "peak_source": peak_src,
-                     # the kernel is not DRAM-bound: its epoch is set by random L2 sector operations
-                     # (one RED per structural nonzero into the column sums + the slack tiles' reads
-                     # of x).  Sector counts from the committed ncu capture, time live.
+                     # the kernel is not DRAM-bound: its epoch is set by random L2 sector reads (x, once per
+                     # structural nonzero from its column's tile and once from its row's slack tile).
+                     # Sector counts from the committed ncu capture, time live.
                      "l2_ops": l2_ops(ep_med)},
         "result": {"lp_obj": ob.lp_obj, "f_beta": ob.f_beta, "max_violation_eps": ob.max_violation_eps,
                    "drift_inf": ob.drift_inf, "cover_cost": rr.cost, "feasible": int(rr.feasible),

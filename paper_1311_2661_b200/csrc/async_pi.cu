@@ -24,16 +24,19 @@
 // A hub is thus gathered at its position within microseconds by many warps and its
 // step reaches r G positions later: a bounded delay, the async model of P:463-476.
 //
-// Edge-incidence LPs (VC / MIS: every row is x_u + x_v -/+ s_i = 1) run the same order in
+// Edge-incidence LPs (VC / MIS: every row is x_u + x_v + sigma_i s_i = 1) run the same order in
 // the *column-sum form* (kGD, R-23): instead of the m residuals the kernel keeps
-// the n column sums D_u = a_u^T r current (fp64, red.global.add.f64).  A vertex tile reads
-// its D_u (coalesced), steps, and adds its step to the D of its neighbours (one RED per
-// nonzero; no gather); a slack tile forms r_i = x_u + x_v -/+ s_i - 1 from x (one coalesced
-// read of its 32 edges, two L2 reads of x) and adds its step to D_u and D_v.  r itself is
-// not touched during the epochs and is recomputed from z on return (r = A z - b, the A2
-// kernel).  Why: Alg. 1's order makes every nonzero a random access; on r (4 B x 1.05e9
-// rows, uniformly accessed) nearly all of them miss the 126 MB L2, on x and D (n values,
+// per-vertex state -- x by degree rank and the slack sums S_u = sum_i sigma_i s_i (fp64,
+// red.global.add.f64) -- and forms D_u = a_u^T r = deg_u (x_u - 1) + sum_w x_w + S_u at u's
+// turn.  A vertex tile gathers its neighbours' x (one random read per nonzero, no scatter: a
+// step is visible through x); a slack tile forms r_i = x_u + x_v + sigma s_i - 1 from x (one
+// coalesced read of its 32 rows' endpoint slots, two L2 reads of x) and adds its step to S_u
+// and S_v.  r itself is not touched during the epochs and is recomputed from z on return
+// (r = A z - b, the A2 kernel).  Why: Alg. 1's order makes every nonzero a random access; on r
+// (4 B x 1.05e9 rows, uniformly accessed) nearly all of them miss the 126 MB L2, on x (n values,
 // accessed in proportion to degree) the hot set of a power-law graph is L2-resident.
+// THETIS_GD_PULL=0 builds the earlier push form (D_u maintained, every step pushed into the
+// neighbours' D with one RED per nonzero: bound by the L2's atomic rate).
 //
 // Work distribution: slot batches of kPiBatch; batch b belongs to CTA b mod gridDim,
 // whose warps draw that CTA's batches in order from a shared-memory counter, so all

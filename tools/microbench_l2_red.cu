@@ -18,6 +18,22 @@ __global__ void k_red64(double* acc, int64_t n_acc, int64_t ops, uint64_t seed) 
         atomicAdd(acc + (h % n_acc), 1.0);
     }
 }
+// random 4-byte reads (ld.global.cg: L2 only) of an L2-resident array, eight in flight per thread
+__global__ void k_read(const float* acc, int64_t n_acc, int64_t ops, uint64_t seed, float* out) {
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    float s = 0;
+    for (int64_t i = tid; i < ops; i += 8 * nt) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            uint64_t h = (i + q * nt + seed) * 0x9E3779B97F4A7C15ULL; h ^= h >> 29; h *= 0xBF58476D1CE4E5B9ULL; h ^= h >> 32;
+            asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v[q]) : "l"(acc + (h % n_acc)));
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) s += v[q];
+    }
+    if (s == 12345.f) *out = s;
+}
 __global__ void k_stream(const float4* a, int64_t n, float* out) {
     float s = 0; int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < n; i += nt) { float4 v = a[i]; s += v.x + v.y + v.z + v.w; }
@@ -42,6 +58,15 @@ int main() {
             float ms64; cudaEventElapsedTime(&ms64, e0, e1);
             printf("red.f64 random %lld MB: blocks %d  %.2f ms  %.1f G/s\n", (long long)mb, 148 * 32, ms64, ops / ms64 / 1e6);
             cudaFree(acc64);
+        }
+        for (int64_t mb : {22, 48}) {
+            const int64_t nr = (mb << 20) >> 2;
+            float* accr; cudaMalloc(&accr, nr * 4); cudaMemset(accr, 0, nr * 4);
+            k_read<<<148 * 32, 256>>>(accr, nr, ops / 8, 99, acc);  // warm the L2
+            cudaEventRecord(e0); k_read<<<148 * 32, 256>>>(accr, nr, ops, it, acc); cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float msr; cudaEventElapsedTime(&msr, e0, e1);
+            printf("ld.cg.f32 random %lld MB: blocks %d  %.2f ms  %.1f G/s\n", (long long)mb, 148 * 32, msr, ops / msr / 1e6);
+            cudaFree(accr);
         }
         cudaEventRecord(e0); k_stream<<<148 * 8, 256>>>((float4*)a, big / 16, acc); cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
