@@ -91,7 +91,7 @@ struct PiCtx {
     const int32_t* nbr;               // rank of the neighbour of CSC entry t
     const int2* erank;                // ranks of the endpoints of row i
     float* xr;                        // x by rank (kept current)
-    double* Dg;                       // column sums D_u = a_u^T r by rank (fp64, kept current)
+    double* Dg;                       // by rank, fp64, kept current: the slack sums S_u (pull form) or D_u (push form)
     int64_t hot;                      // slots below this are kept in L2 (evict_last)
 };
 
@@ -114,9 +114,6 @@ __device__ __forceinline__ int atom_add_release(int32_t* p, int v) {
     return old;
 }
 
-__device__ __forceinline__ void red_add_f64(double* p, double v) {
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
 __device__ __forceinline__ double ld_cg_f64(const double* p) {
     double v;
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -231,7 +228,7 @@ __device__ __forceinline__ float slack_lane_gather(const DevLP& L, const StepPar
     return sig < 0.0f ? -d : d;
 }
 
-// column-sum form (VC / MIS): the slack of row q = (u, v) from x; its step enters D_u and D_v
+// column-sum form (VC / MIS): the slack of row q = (u, v) from x; its step enters the sums of u and v
 __device__ __forceinline__ void slack_lane_gd(const DevLP& L, const StepParams& P, const PiCtx& C, const L2Pol& pol,
                                               int64_t q) {
     const int64_t j = L.n_s + q;
@@ -834,7 +831,7 @@ __global__ void k_fill_erank(DevLP L, const int32_t* __restrict__ rank, int2* __
         erank[i] = make_int2(rank[e.x], rank[e.y]);
     }
 }
-// per call: x by rank, and D_u = a_u^T r from the rows (r = A z - b on entry): r_i into both endpoints
+// per call: x by rank, and the maintained sums from the rows (both endpoints of each)
 __global__ void k_init_xr(DevLP L, const int32_t* __restrict__ rank, float* __restrict__ xr) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < L.n_s; u += (int64_t)gridDim.x * blockDim.x)
         xr[rank[u]] = L.z[u];

@@ -345,7 +345,7 @@ struct thetis_lp {
     int32_t* nbr = nullptr;        // rank of the neighbour of CSC entry t (the other endpoint of its row)
     int2* erank = nullptr;         // ranks of the endpoints of row i
     float* xr = nullptr;           // x by rank (a copy of z[0, n) kept current during the epochs)
-    double* Dg = nullptr;          // column sums D_u = a_u^T r by rank, kept current during the epochs
+    double* Dg = nullptr;          // per-vertex sums by rank kept current during the epochs (S_u = sum sigma s; R-23)
     bool nbr_valid = false;
     double maxnorm2 = 0;           // max_j ||a_j||^2 over all standard-form columns
     int64_t epoch_updates = 0;     // coordinates updated per epoch (stats)
